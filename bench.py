@@ -1,0 +1,398 @@
+#!/usr/bin/env python
+"""Benchmark: BFS GTEPS (harmonic mean over seeded roots) on the RCM-reordered
+Kronecker graph of BASELINE.json configs[1] (scale 22, edgefactor 16).
+
+A "step" is one BFS traversal from one seeded root (the reference's
+BfsEngine.run, engine.py:518-604) over the HBM-resident RCM graph.  The
+headline per-root TEPS numerator is the raw input pairs in the root's
+component (bench.py:186-189, 336-338 of the reference; the paper's
+convention); the dedup numerator (traversed edges) is reported alongside.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--scale S] [--impl ours|reference]
+
+Rank 0 prints ONE JSON line.  ``--impl reference`` times the CPU reference
+path (the oracle port of BfsEngine hybrid mode, C + OpenMP on all host
+cores) on the same config -- it never touches the CUDA library.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "BFS GTEPS (harmonic mean, 64 roots) on RCM-reordered Kronecker graphs"
+UNIT = "GTEPS"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=64)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--scale", type=int, default=22)
+    ap.add_argument("--edgefactor", type=int, default=16)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--mode", default="hybrid")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-roots", type=int, default=0, help="only run N roots (for ncu)")
+    return ap.parse_args()
+
+
+def hmean(x):
+    x = np.asarray(x, dtype=np.float64)
+    return float(x.size / np.sum(1.0 / x))
+
+
+# ---------------------------------------------------------------------------
+# byte model, per root, from the level records
+
+
+def algorithmic_bytes(levels, n_dev: int, n_plus_dev: int) -> int:
+    """TD level: |F|*(4 queue + 16 offsets) + 4*E_TD + n_next*(4 parent + 4 queue + 4 level)
+    BU level: 3*(n_dev/8) + 8*U + 4*C + n_next*(4 parent + 4 level)."""
+    total = 0
+    reached = 0
+    for i, r in enumerate(levels):
+        reached += r.n_f
+        n_next = levels[i + 1].n_f if i + 1 < len(levels) else 0
+        if r.direction == "top_down":
+            total += r.n_f * 20 + 4 * r.scanned_edges + n_next * 12
+        else:
+            U = max(n_plus_dev - reached, 0)
+            total += 3 * (n_dev // 8) + 8 * U + 4 * r.scanned_edges + n_next * 8
+    return int(total)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                    capture_output=True, text=True, timeout=5,
+                ).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 2 + i and s[2 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def load_traffic():
+    try:
+        with open(os.path.join(ROOT, "profiles", "roofline_traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm (oracle port of BfsEngine hybrid, all host cores)
+
+
+def cpu_graph(scale, edgefactor, seed):
+    import oracle
+
+    t0 = time.perf_counter()
+    n, e = oracle.kronecker_generate(scale, edgefactor, seed=seed)
+    t1 = time.perf_counter()
+    g = oracle.build_csr(n, e)
+    t2 = time.perf_counter()
+    perm, n_plus, ranges = oracle.rcm(g)
+    g2 = oracle.apply_permutation(g, perm)
+    t3 = time.perf_counter()
+    inv = oracle.inverse(perm)
+    return dict(n=n, edges=e, g2=g2, perm=perm, inv=inv, n_plus=n_plus, ranges=ranges,
+                timings={"generate_s": t1 - t0, "csr_build_s": t2 - t1, "rcm_s": t3 - t2})
+
+
+def raw_pairs_for(ranges, inv, edges, roots):
+    """Raw input pairs whose first endpoint lies in each root's component."""
+    starts = np.array([a for a, _ in ranges], np.int64)
+    lab_u = inv[edges[:, 0]].astype(np.int64)
+    out = []
+    cache = {}
+    for s in roots:
+        ci = int(np.searchsorted(starts, s, side="right") - 1)
+        if ci not in cache:
+            a, b = ranges[ci]
+            cache[ci] = int(np.count_nonzero((lab_u >= a) & (lab_u < b)))
+        out.append(cache[ci])
+    return np.array(out, np.int64)
+
+
+def cpu_bfs_sample(cg, roots, raw, seconds, threads=0):
+    """Time the oracle hybrid BFS on roots until `seconds` elapse (>=1 root)."""
+    import oracle
+
+    g2 = cg["g2"]
+    oracle.hybrid_bfs(g2, int(roots[0]), threads=threads)  # warm-up (reference has none; cold caches hurt)
+    teps, used = [], 0
+    t_start = time.perf_counter()
+    for s, rp in zip(roots, raw):
+        _, rec, el = oracle.hybrid_bfs(g2, int(s), threads=threads)
+        teps.append(rp / el)
+        used += 1
+        if time.perf_counter() - t_start > seconds:
+            break
+    return hmean(teps) / 1e9, used
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+
+    oracle.build()
+    threads = os.cpu_count() or 1
+    cg = cpu_graph(args.scale, args.edgefactor, args.seed)
+    roots = oracle.sample_sources(cg["g2"].degrees, 64, 1)
+    raw = raw_pairs_for(cg["ranges"], cg["inv"], cg["edges"], roots)
+    for s in roots[: args.warmup]:
+        oracle.hybrid_bfs(cg["g2"], int(s), threads=threads)
+    teps, times = [], []
+    k = min(args.steps, len(roots))
+    t0 = time.perf_counter()
+    for s, rp in zip(roots[:k], raw[:k]):
+        _, _, el = oracle.hybrid_bfs(cg["g2"], int(s), threads=threads)
+        teps.append(rp / el)
+        times.append(el)
+    wall = time.perf_counter() - t0
+    v = hmean(teps) / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": k,
+        "warmup": args.warmup, "ms_per_step": 1e3 * wall / k, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int32", "data": "synthetic Kronecker (reference generator, seed 1)",
+        "config": {"workload": f"kronecker-s{args.scale}-ef{args.edgefactor}-rcm-bfs", "scale": args.scale,
+                   "edgefactor": args.edgefactor, "roots": k, "mode": "hybrid"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{k} seeded roots of the scale-{args.scale} RCM graph, oracle C port of "
+                                   f"BfsEngine hybrid (td_plain + bu_range), OpenMP {threads} threads"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "preprocessing_s": cg["timings"],
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+
+def run_ours(args):
+    import torch
+
+    import paper_2012_10026_b200 as rb
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    # ---- preprocessing (timed separately, reported, not part of the metric)
+    t0 = time.perf_counter()
+    el = rb.kronecker_generate(rb.KroneckerParams(scale=args.scale, edgefactor=args.edgefactor, seed=args.seed))
+    t_gen = time.perf_counter() - t0
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    g = rb.build_csr(el)
+    torch.cuda.synchronize()
+    t_csr = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    perm, stats = rb.rcm(g)
+    g2 = rb.apply_permutation(g, perm)
+    torch.cuda.synchronize()
+    t_rcm = time.perf_counter() - t0
+    del g
+
+    # roots (bench.py:124-134) and raw pairs per root component
+    deg2 = g2.device_arrays()[2]
+    roots = rb.sample_sources(deg2.cpu().numpy(), 64, 1)
+    inv_t = perm.device_arrays()[1]
+    e_t = torch.from_numpy(el.edges[:, 0].view(np.int32)).cuda()
+    lab = inv_t[e_t.long()].long()
+    starts = np.array([a for a, _ in stats.component_ranges], np.int64)
+    raw_cache, raw = {}, []
+    for s in roots:
+        ci = int(np.searchsorted(starts, s, side="right") - 1)
+        if ci not in raw_cache:
+            a, b = stats.component_ranges[ci]
+            raw_cache[ci] = int(((lab >= a) & (lab < b)).sum().item())
+        raw.append(raw_cache[ci])
+    raw = np.array(raw, np.int64)
+    del e_t, lab
+
+    eng = rb.BfsEngine(g2, rb.BfsParams(mode=args.mode))
+    n_dev = eng.n_dev
+    n_plus_dev = stats.n_non_isolated
+    # this rank's roots (replicas: roots are dealt round-robin over ranks)
+    order = np.arange(64)
+    k = args.steps if args.profile_roots == 0 else args.profile_roots
+    my = [order[(rank + world * i) % 64] for i in range(k)]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+
+    for i in range(args.warmup if args.profile_roots == 0 else 1):
+        eng.run_device(int(roots[my[i % len(my)]]))
+    torch.cuda.synchronize()
+
+    times, teps, teps_dedup, bytes_alg, lvl_counts = [], [], [], [], []
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev_a = torch.cuda.Event(enable_timing=True)
+    ev_b = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev_a.record()
+        for j in my:
+            flush.zero_()
+            el_s, levels = eng.run_device(int(roots[j]))
+            times.append(el_s)
+            teps.append(raw[j] / el_s)
+            teps_dedup.append((sum(r.m_f for r in levels) // 2) / el_s)
+            bytes_alg.append(algorithmic_bytes(levels, n_dev, n_plus_dev))
+            lvl_counts.append(len(levels))
+        ev_b.record()
+        torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    wall_ms = ev_a.elapsed_time(ev_b)
+
+    # ---- e2e through the public API: BfsEngine.run -> host predecessor array
+    e2e_teps = []
+    for j in my[: min(len(my), 16)]:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = eng.run(int(roots[j]))
+        dt = time.perf_counter() - t0
+        e2e_teps.append(raw[j] / dt)
+    d2h = 4 * n_dev + 64 * len(res.levels)
+
+    value_rank = hmean(teps) / 1e9
+    ms_rank = 1e3 * float(np.mean(times))
+    if dist is not None:
+        t = torch.tensor([value_rank, ms_rank, hmean(e2e_teps) / 1e9], device="cuda", dtype=torch.float64)
+        vals = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(vals, t)
+        vals = torch.stack(vals).cpu().numpy()
+        value = float(vals[:, 0].sum())  # replicas: aggregate traversal throughput
+        ms = float(vals[:, 1].max())
+        e2e_v = float(vals[:, 2].sum())
+    else:
+        value, ms, e2e_v = value_rank, ms_rank, hmean(e2e_teps) / 1e9
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    peak, peak_kind = measured_peak()
+    ach = float(np.sum(bytes_alg) / np.sum(times) / 1e9)
+    traffic = load_traffic()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": len(my), "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic Kronecker (reference generator, seed 1), built on device",
+        "config": {"workload": f"kronecker-s{args.scale}-ef{args.edgefactor}-rcm-bfs", "scale": args.scale,
+                   "edgefactor": args.edgefactor, "roots": len(my), "mode": args.mode,
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "flushed (256 MiB write) before every root", "n": int(g2.n), "n_plus": int(n_plus_dev),
+                   "m_directed": int(g2.m_directed)},
+        "gteps_dedup_hmean": hmean(teps_dedup) / 1e9,
+        "gteps_min": float(np.min(teps)) / 1e9, "gteps_max": float(np.max(teps)) / 1e9,
+        "depth_median": float(np.median(lvl_counts)) - 1,
+        "preprocessing_s": {"generate_host": t_gen, "csr_build": t_csr, "rcm_plus_relabel": t_rcm},
+        "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                     "peak_kind": peak_kind, "kernel": "bfs_persistent",
+                     "bytes_per_launch": float(np.mean(bytes_alg)),
+                     "launch_ms": 1e3 * float(np.mean(times)),
+                     "traffic": None if traffic is None else traffic.get("bytes_per_launch")},
+        "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": 8, "d2h_bytes_per_step": int(d2h),
+                "api": "BfsEngine.run(source) -> BfsResult with host predecessor"},
+        "gpu_launches": int(len(my) * 2),  # bfs_seed + bfs_persistent per root
+        "clocks": clk.summary(),
+        "timed_wall_ms": wall_ms,
+    }
+    if not args.no_cpu_baseline and args.profile_roots == 0:
+        try:
+            import oracle
+
+            oracle.build()
+            go = oracle.Csr(g2.n, g2.row_starts, g2.dst, g2.degrees)
+            threads = os.cpu_count() or 1
+            v, used = cpu_bfs_sample({"g2": go}, roots, raw, args.cpu_seconds, threads=threads)
+            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                                    "sample": f"{used} seeded roots of the same RCM graph, oracle C port of "
+                                              f"BfsEngine hybrid, OpenMP {threads} threads"}
+        except Exception as ex:  # pragma: no cover
+            line["cpu_baseline"] = {"value": None, "error": repr(ex)}
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

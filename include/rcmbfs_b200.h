@@ -1,0 +1,112 @@
+/*
+ * rcmbfs_b200.h -- C ABI of the B200-native RCM + direction-optimizing BFS.
+ *
+ * The reference package (rcmbfs, /root/reference/pkg/src/rcmbfs) has no FFI;
+ * its drop-in boundary is the public Python surface (__init__.py:12-105).
+ * These entry points are what that surface binds to (see INTEGRATION.md for
+ * the ctypes binding).  Every pointer named d_* is a caller-owned DEVICE
+ * pointer on the current device; h_* pointers are host memory; stream is a
+ * cudaStream_t passed as void*.  Return codes: RB_OK, RB_ERR_ARG (the shim
+ * raises ValueError with the reference's message), RB_ERR_CUDA, RB_ERR_OOM.
+ * rb_last_error() gives a thread-local message for the last failure.
+ */
+#ifndef RCMBFS_B200_H
+#define RCMBFS_B200_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { RB_OK = 0, RB_ERR_ARG = 1, RB_ERR_CUDA = 2, RB_ERR_NCCL = 3, RB_ERR_OOM = 4 };
+
+const char* rb_last_error(void);
+int rb_version(void);
+
+/* ---- CSR build: replaces graph.py:85-120 (build_csr) -------------------- */
+/* Stage 1 (sizes + error check).  d_edges: m_raw (u,v) uint32 pairs.
+ * On an out-of-range edge returns RB_ERR_ARG with *bad_index = first index.
+ * ws: workspace of rb_csr_workspace_bytes(m_raw, n) bytes.
+ * On success *m_directed = deduplicated directed edge count and the sorted
+ * unique keys are kept in ws for stage 2. */
+size_t rb_csr_workspace_bytes(int64_t m_raw, int64_t n);
+int rb_csr_build(const uint32_t* d_edges, int64_t m_raw, int64_t n, void* d_ws, size_t ws_bytes,
+                 int64_t* m_directed, int64_t* bad_index, void* stream);
+/* Stage 2: materialize CSR from ws (row_starts n+1 int64, col m_directed
+ * int32, degrees n int32). */
+int rb_csr_emit(const void* d_ws, int64_t m_directed, int64_t n, int64_t* d_row_starts,
+                int32_t* d_col, int32_t* d_degrees, void* stream);
+
+/* ---- RCM: replaces reorder.py:198-237 (rcm / _rcm_impl / _rcm_walk) ----- */
+/* Outputs perm (new->old) and inv (old->new), |V+|, component ranges (pairs of
+ * new-id [start,end), ascending by start; capacity n pairs).  Bit-exact with
+ * the reference's sequential walk. */
+size_t rb_rcm_workspace_bytes(int64_t n, int64_t m_directed);
+int rb_rcm(const int64_t* d_row_starts, const int32_t* d_col, const int32_t* d_degrees, int64_t n,
+           void* d_ws, size_t ws_bytes, uint32_t* d_perm, uint32_t* d_inv, int64_t* n_plus,
+           int64_t* d_comp_ranges, int64_t* n_components, void* stream);
+
+/* ---- relabel: replaces reorder.py:254-271 (apply_permutation) ----------- */
+size_t rb_permute_workspace_bytes(int64_t n, int64_t m_directed);
+int rb_apply_permutation(const int64_t* d_row_starts, const int32_t* d_col, const int32_t* d_degrees,
+                         int64_t n, int64_t m_directed, const uint32_t* d_perm, const uint32_t* d_inv,
+                         void* d_ws, size_t ws_bytes, int64_t* d_row_starts_out, int32_t* d_col_out,
+                         int32_t* d_degrees_out, void* stream);
+/* degree_sort_adjacency (reorder.py:151-195): rows re-sorted by (deg, id)
+ * ascending or by (deg desc, id asc). */
+int rb_degree_sort_adjacency(const int64_t* d_row_starts, const int32_t* d_col, const int32_t* d_degrees,
+                             int64_t n, int64_t m_directed, int descending, void* d_ws, size_t ws_bytes,
+                             int32_t* d_col_out, void* stream);
+
+/* ---- BFS engine: replaces engine.py:478-617 (BfsEngine / bfs_run) ------- */
+typedef struct rb_bfs rb_bfs;
+
+typedef struct {
+  int64_t level;
+  int64_t direction; /* 0 = top_down, 1 = bottom_up */
+  int64_t n_f;
+  int64_t m_f;
+  int64_t m_u;
+  int64_t scanned_edges; /* TD: edges examined; BU: neighbour checks */
+  int64_t t_ns;          /* device %globaltimer duration of the level */
+  int64_t n_next;
+} rb_level_record;
+
+typedef struct {
+  int32_t alpha;      /* engine.py:85 */
+  int32_t beta;       /* engine.py:86 */
+  int32_t hybrid;     /* 0 = level_sync (top-down only) */
+  int32_t bu_reverse; /* scan bottom-up rows from their end */
+  int64_t n_policy;   /* g.n incl. isolated (engine.py:593) */
+  int64_t m_directed; /* g.m_directed */
+} rb_bfs_params;
+
+/* d_col_bu may equal d_col.  n_dev: vertices [0,n_dev) live on the device
+ * (isolated tail dropped); d_isolated_words marks isolated vertices inside
+ * [0,n_dev) (uint32 words, bit v -> word v>>5), may be NULL. */
+int rb_bfs_create(const int64_t* d_row_starts, const int32_t* d_col, const int32_t* d_col_bu,
+                  const int32_t* d_degrees, int64_t n_dev, const uint32_t* d_isolated_words,
+                  const rb_bfs_params* params, rb_bfs** out);
+int rb_bfs_destroy(rb_bfs* h);
+/* Reset per-root state (not timed; engine.py:526-532). */
+int rb_bfs_reset(rb_bfs* h, int64_t source, void* stream);
+/* The traversal (engine.py:534-598): one cooperative persistent launch. */
+int rb_bfs_traverse(rb_bfs* h, void* stream);
+/* Copy results; parents/levels cover [0,n_dev); n_records <= cap. */
+int rb_bfs_results(rb_bfs* h, int32_t* d_or_h_parent, int32_t* d_or_h_level, rb_level_record* h_records,
+                   int64_t cap, int64_t* n_records, void* stream);
+/* One step from an explicit state (top_down_step / bottom_up_step,
+ * engine.py:252-429): state words are uint32 over [0,n_dev). */
+int rb_bfs_step(rb_bfs* h, int direction, const uint32_t* d_visited_words, const uint32_t* d_frontier_words,
+                const int32_t* d_parent_in, uint32_t* d_visited_out, uint32_t* d_next_out,
+                int32_t* d_parent_out, int64_t* h_counters /* n_next, deg_next, scanned */, void* stream);
+/* Device pointers of the engine-owned parent / level arrays. */
+int32_t* rb_bfs_parent_ptr(rb_bfs* h);
+int32_t* rb_bfs_level_ptr(rb_bfs* h);
+int rb_bfs_grid(rb_bfs* h, int* blocks, int* threads);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

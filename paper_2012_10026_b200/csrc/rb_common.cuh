@@ -1,0 +1,97 @@
+// rb_common.cuh -- shared device helpers for the B200 RCM + BFS kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define RB_FULL 0xffffffffu
+
+namespace rb {
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const unsigned long long* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Read-only (for the whole launch) streaming loads of graph structure.
+__device__ __forceinline__ int32_t ldg_i32(const int32_t* p) { return __ldg(p); }
+__device__ __forceinline__ int64_t ldg_i64(const int64_t* p) { return __ldg(p); }
+
+// Grid-wide barrier for a cooperative (co-resident) launch.  bar[0] = arrival
+// count, bar[1] = generation.  Release/acquire at gpu scope orders every
+// block's global writes before any block proceeds.
+__device__ __forceinline__ void grid_barrier(uint32_t* bar, uint32_t nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t gen = ld_acquire_u32(bar + 1);
+    __threadfence();
+    uint32_t arrived = atomicAdd(bar, 1u);
+    if (arrived == nblocks - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (ld_acquire_u32(bar + 1) == gen) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+
+// Warp inclusive scan (32-bit).
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
+  const uint32_t lane = lane_id();
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(RB_FULL, x, o);
+    if (lane >= (uint32_t)o) x += y;
+  }
+  return x;
+}
+
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(RB_FULL, x, o);
+  return x;
+}
+
+// First lane j whose inclusive prefix incl[j] > e (incl nondecreasing, e < incl[31]).
+__device__ __forceinline__ uint32_t warp_upper_bound(uint32_t incl, uint32_t e) {
+  uint32_t j = 0;
+#pragma unroll
+  for (uint32_t s = 16; s >= 1; s >>= 1) {
+    uint32_t v = __shfl_sync(RB_FULL, incl, j + s - 1);
+    if (v <= e) j += s;
+  }
+  return j;
+}
+
+__device__ __forceinline__ int64_t shfl_i64(int64_t v, int src) {
+  return (int64_t)__shfl_sync(RB_FULL, (long long)v, src);
+}
+
+}  // namespace rb
+
+#define RB_CUDA_TRY(x)                                  \
+  do {                                                  \
+    cudaError_t _e = (x);                               \
+    if (_e != cudaSuccess) {                            \
+      rb_set_error("%s:%d %s: %s", __FILE__, __LINE__,  \
+                   #x, cudaGetErrorString(_e));         \
+      return RB_ERR_CUDA;                               \
+    }                                                   \
+  } while (0)

@@ -1,0 +1,492 @@
+"""Direction-optimizing BFS engine on B200 (reference engine.py:1-639).
+
+Same public surface as the reference (``BfsParams``, ``BfsEngine``,
+``bfs_run``, the step functions, ``update_traversal_policy``...), but every
+traversal runs on the device through the C ABI (include/rcmbfs_b200.h):
+
+* ``BfsEngine.run`` = reset (untimed, engine.py:526-532) + ONE cooperative
+  persistent kernel for the whole level loop (engine.py:534-598) + copy-out.
+  The per-level direction policy runs on device with exactly
+  ``update_traversal_policy``'s arithmetic (n = g.n including isolated).
+* Isolated vertices beyond the last non-isolated id are dropped from the
+  device state (after RCM they are the tail [|V+|, n)); isolated vertices
+  inside the range are premarked visited (engine.py:432-437).
+* Modes: ``hybrid`` / ``hybrid_balanced`` scan bottom-up rows from their end
+  (RCM ids ascend with degree); ``hybrid_reduced`` scans the descending-degree
+  adjacency ``g_desc`` forward (Alg. 6 order); ``level_sync`` and
+  ``sequential`` are top-down only.  Parents may differ from the CPU
+  reference's (any valid BFS tree); levels, per-level n_f / m_f / m_u and
+  directions are identical.
+
+There is no CPU fallback: constructing an engine without CUDA raises.
+"""
+
+from __future__ import annotations
+
+import csv
+import ctypes
+import os
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .bitmap import Bitmap
+from .graph import CsrGraph
+
+__all__ = [
+    "TOP_DOWN", "BOTTOM_UP", "MODES", "BfsParams", "Frontier", "StepStats", "LevelRecord", "BfsResult",
+    "PolicyCounters", "update_traversal_policy", "default_partition_factor", "top_down_step",
+    "top_down_step_balanced", "bottom_up_step", "bottom_up_step_balanced", "bottom_up_step_reduced",
+    "bfs_sequential", "bfs_run", "BfsEngine", "write_level_trace",
+]
+
+TOP_DOWN = "top_down"
+BOTTOM_UP = "bottom_up"
+MODES = ("sequential", "level_sync", "hybrid", "hybrid_balanced", "hybrid_reduced")
+
+
+def default_partition_factor(n: int) -> int:
+    """engine.py:70-72."""
+    return 10 if n < (1 << 26) else 20
+
+
+@dataclass
+class BfsParams:
+    """Traversal configuration (engine.py:75-103), same validation."""
+
+    alpha: int = 64
+    beta: int = 8
+    partition_factor: int = 20
+    threads: int = 1
+    mode: str = "hybrid"
+
+    def __post_init__(self):
+        if not 1 <= self.alpha <= 128:
+            raise ValueError(f"alpha must be in [1, 128], got {self.alpha}")
+        if not 1 <= self.beta <= 32:
+            raise ValueError(f"beta must be in [1, 32], got {self.beta}")
+        if self.partition_factor < 1:
+            raise ValueError(f"partition_factor must be >= 1, got {self.partition_factor}")
+        if self.threads < 1:
+            raise ValueError(f"threads must be >= 1, got {self.threads}")
+        if self.mode not in MODES:
+            raise ValueError(f"mode must be one of {MODES}, got {self.mode!r}")
+
+
+@dataclass
+class Frontier:
+    """One level's vertex set in queue and/or bitmap form (engine.py:106-151)."""
+
+    n: int
+    queue: np.ndarray | None = None
+    bits: Bitmap | None = None
+    active: str = "queue"
+
+    @classmethod
+    def from_queue(cls, n: int, queue: np.ndarray) -> "Frontier":
+        return cls(n=n, queue=np.ascontiguousarray(queue, dtype=np.uint32), active="queue")
+
+    @classmethod
+    def from_bitmap(cls, bits: Bitmap) -> "Frontier":
+        return cls(n=bits.n_bits, bits=bits, active="bitmap")
+
+    @property
+    def count(self) -> int:
+        if self.queue is not None:
+            return int(self.queue.size)
+        return self.bits.count()
+
+    def indices(self) -> np.ndarray:
+        if self.queue is not None:
+            return self.queue
+        return self.bits.to_indices()
+
+    def to_queue_form(self) -> "Frontier":
+        if self.queue is not None:
+            return self
+        return Frontier(n=self.n, queue=self.bits.to_indices(), bits=self.bits, active="queue")
+
+    def to_bitmap_form(self) -> "Frontier":
+        if self.bits is not None:
+            return self
+        return Frontier(n=self.n, queue=self.queue, bits=Bitmap.from_indices(self.n, self.queue), active="bitmap")
+
+
+@dataclass
+class StepStats:
+    n_next: int
+    deg_next: int
+    scanned_edges: int
+    per_thread_edges: np.ndarray
+    pass1_hits: int | None = None
+    claimed: int | None = None
+
+
+@dataclass
+class LevelRecord:
+    """Per-level trace entry (engine.py:166-180); wall_time is device time."""
+
+    level: int
+    direction: str
+    n_f: int
+    m_f: int
+    m_u: int
+    scanned_edges: int
+    wall_time: float
+    per_thread_edges: np.ndarray | None = None
+    pass1_hits: int | None = None
+    live_vertices: int | None = None
+    claimed: int | None = None
+
+
+@dataclass
+class BfsResult:
+    source: int
+    n: int
+    predecessor: np.ndarray
+    levels: list
+    elapsed_time: float
+    traversed_edges: int
+    mode: str
+
+    @property
+    def depth(self) -> int:
+        return len(self.levels) - 1
+
+    @property
+    def n_reached(self) -> int:
+        return int(np.count_nonzero(self.predecessor >= 0))
+
+
+@dataclass
+class PolicyCounters:
+    direction: str
+    m_f: int
+    m_u: int
+    n_f: int
+    n: int
+
+
+def update_traversal_policy(counters: PolicyCounters, params: BfsParams) -> str:
+    """engine.py:215-228 (the device kernel evaluates the same expression)."""
+    if counters.direction == TOP_DOWN:
+        if counters.m_f > counters.m_u / params.alpha:
+            return BOTTOM_UP
+        return TOP_DOWN
+    if counters.n_f < counters.n / params.beta:
+        return TOP_DOWN
+    return BOTTOM_UP
+
+
+def _split_even(total: int, parts: int) -> np.ndarray:
+    """Device work reported as `parts` equal shares (per_thread_edges field)."""
+    return np.array([total * (k + 1) // parts - total * k // parts for k in range(parts)], dtype=np.int64)
+
+
+# ---------------------------------------------------------------------------
+# device engine handle
+
+
+class _DeviceBfs:
+    """Owns one rb_bfs handle: graph views + device traversal state."""
+
+    def __init__(self, g: CsrGraph, *, hybrid: bool, alpha: int, beta: int, g_bu: CsrGraph | None,
+                 bu_reverse: bool, trim_isolated: bool):
+        torch = _lib.require_cuda()
+        self.torch = torch
+        L = _lib.lib()
+        self.g = g
+        rs, col, deg = g.device_arrays()
+        self._keep = [rs, col, deg]
+        n = g.n
+        if trim_isolated:
+            nz = torch.nonzero(deg > 0)
+            n_dev = int(nz.max().item()) + 1 if nz.numel() else 0
+        else:
+            n_dev = n
+        self.n_dev = n_dev
+        self.h = ctypes.c_void_p(0)
+        if n_dev == 0:
+            return
+        iso = None
+        if trim_isolated:
+            nw = (n_dev + 31) // 32
+            flags = torch.zeros(nw * 32, dtype=torch.int64, device="cuda")
+            flags[:n_dev] = (deg[:n_dev] == 0).to(torch.int64)
+            shifts = torch.arange(32, device="cuda", dtype=torch.int64)
+            words = (flags.view(nw, 32) << shifts).sum(dim=1)
+            iso = torch.where(words >= (1 << 31), words - (1 << 32), words).to(torch.int32)  # uint32 bit pattern
+            self._keep.append(iso)
+        col_bu = col
+        if g_bu is not None:
+            col_bu = g_bu.device_arrays()[1]
+            self._keep.append(col_bu)
+        prm = _lib.BfsParamsC(alpha, beta, int(hybrid), int(bu_reverse), n, g.m_directed)
+        _lib.check(
+            L.rb_bfs_create(_lib.ptr(rs), _lib.ptr(col), _lib.ptr(col_bu), _lib.ptr(deg), n_dev,
+                            _lib.ptr(iso) if iso is not None else None, ctypes.byref(prm), ctypes.byref(self.h)),
+            "rb_bfs_create",
+        )
+        self.pinned = torch.empty(n_dev, dtype=torch.int32, pin_memory=True)
+        self.ev0 = torch.cuda.Event(enable_timing=True)
+        self.ev1 = torch.cuda.Event(enable_timing=True)
+
+    def close(self):
+        if self.h:
+            _lib.lib().rb_bfs_destroy(self.h)
+            self.h = ctypes.c_void_p(0)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def traverse(self, source: int):
+        """Reset + timed traversal; returns device seconds."""
+        L = _lib.lib()
+        s = _lib.stream_ptr()
+        _lib.check(L.rb_bfs_reset(self.h, int(source), s), "rb_bfs_reset")
+        self.ev0.record()
+        _lib.check(L.rb_bfs_traverse(self.h, s), "rb_bfs_traverse")
+        self.ev1.record()
+
+    def results(self, want_parent=True, want_level=False, level_out=None):
+        L = _lib.lib()
+        cap = 1 << 16
+        recs = (_lib.LevelRecordC * cap)()
+        nrec = ctypes.c_int64(0)
+        lvl = level_out
+        _lib.check(
+            L.rb_bfs_results(self.h, _lib.ptr(self.pinned) if want_parent else None,
+                             _lib.ptr(lvl) if lvl is not None else None, recs, cap, ctypes.byref(nrec),
+                             _lib.stream_ptr()),
+            "rb_bfs_results",
+        )
+        elapsed = self.ev0.elapsed_time(self.ev1) / 1000.0
+        return recs[: min(nrec.value, cap)], elapsed
+
+    def level_tensor(self):
+        """Device int32 level array over [0, n_dev) (valid after results())."""
+        ptr = _lib.lib().rb_bfs_level_ptr(self.h)
+        return ptr
+
+
+def _records_to_levels(recs) -> list:
+    out = []
+    for r in recs:
+        out.append(
+            LevelRecord(
+                level=int(r.level), direction=TOP_DOWN if r.direction == 0 else BOTTOM_UP, n_f=int(r.n_f),
+                m_f=int(r.m_f), m_u=int(r.m_u), scanned_edges=int(r.scanned_edges), wall_time=r.t_ns * 1e-9,
+                per_thread_edges=np.array([int(r.scanned_edges)], dtype=np.int64),
+            )
+        )
+    return out
+
+
+class BfsEngine:
+    """Reusable traversal context (engine.py:478-604): device state per graph."""
+
+    def __init__(self, g: CsrGraph, params: BfsParams, g_desc: CsrGraph | None = None):
+        self.g = g
+        self.params = params
+        self.g_desc = g_desc
+        if params.mode == "hybrid_reduced":
+            if g_desc is None:
+                raise ValueError(
+                    "hybrid_reduced needs the descending-degree adjacency "
+                    "variant (pass g_desc, e.g. degree_sort_adjacency(g))"
+                )
+            if g_desc.n != g.n or g_desc.m_directed != g.m_directed:
+                raise ValueError("g_desc does not match g")
+        self.ps = None
+        self.pool = None  # device engine: no host worker pool
+        hybrid = params.mode not in ("sequential", "level_sync")
+        reduced = params.mode == "hybrid_reduced"
+        self._dev = _DeviceBfs(
+            g, hybrid=hybrid, alpha=params.alpha, beta=params.beta, g_bu=g_desc if reduced else None,
+            bu_reverse=not reduced, trim_isolated=True,
+        )
+        self._deg_dev = g.device_arrays()[2]
+
+    @property
+    def n_dev(self) -> int:
+        return self._dev.n_dev
+
+    def close(self) -> None:
+        if self._dev is not None:
+            self._dev.close()
+
+    def __enter__(self) -> "BfsEngine":
+        return self
+
+    def __exit__(self, *exc) -> None:
+        self.close()
+
+    def _trivial(self, source: int) -> BfsResult:
+        g = self.g
+        pred = np.full(g.n, -1, dtype=np.int32)
+        pred[source] = source
+        rec = LevelRecord(level=0, direction=TOP_DOWN, n_f=1, m_f=0, m_u=g.m_directed, scanned_edges=0,
+                          wall_time=0.0, per_thread_edges=np.zeros(1, np.int64))
+        return BfsResult(source=source, n=g.n, predecessor=pred, levels=[rec], elapsed_time=0.0,
+                         traversed_edges=0, mode=self.params.mode)
+
+    def run(self, source: int) -> BfsResult:
+        g = self.g
+        if not 0 <= source < g.n:
+            raise ValueError(f"source {source} out of range for n={g.n}")
+        source = int(source)
+        if source >= self._dev.n_dev or int(self._deg_dev[source].item()) == 0:
+            return self._trivial(source)
+        self._dev.traverse(source)
+        recs, elapsed = self._dev.results()
+        pred = np.full(g.n, -1, dtype=np.int32)
+        pred[: self._dev.n_dev] = self._dev.pinned.numpy()
+        levels = _records_to_levels(recs)
+        traversed = sum(r.m_f for r in levels) // 2  # = sum deg[reached] // 2 (engine.py:599-600)
+        return BfsResult(source=source, n=g.n, predecessor=pred, levels=levels, elapsed_time=elapsed,
+                         traversed_edges=traversed, mode=self.params.mode)
+
+    # ---- device-resident entry points (bench / parity tests) ------------
+    def run_device(self, source: int, levels_out=None):
+        """Traverse without copying parents to the host.  Returns
+        (device seconds, LevelRecords).  If ``levels_out`` (int32 CUDA
+        tensor of n_dev) is given, the level array is copied into it."""
+        self._dev.traverse(int(source))
+        recs, elapsed = self._dev.results(want_parent=False, level_out=levels_out)
+        return elapsed, _records_to_levels(recs)
+
+    def parent_device(self):
+        """int32 CUDA tensor view of the engine's parent array [0, n_dev)."""
+        return _ptr_view(_lib.lib().rb_bfs_parent_ptr(self._dev.h), self._dev.n_dev)
+
+    def level_device(self):
+        return _ptr_view(_lib.lib().rb_bfs_level_ptr(self._dev.h), self._dev.n_dev)
+
+
+def _ptr_view(ptr: int, n: int):
+    """Non-owning int32 CUDA tensor over an engine buffer."""
+    import torch
+
+    class _Holder:
+        __cuda_array_interface__ = {
+            "shape": (n,), "typestr": "<i4", "data": (int(ptr), False), "version": 3, "strides": None,
+        }
+
+    return torch.as_tensor(_Holder(), device="cuda")
+
+
+def bfs_run(g: CsrGraph, source: int, params: BfsParams | None = None, g_desc: CsrGraph | None = None) -> BfsResult:
+    """One-shot traversal (engine.py:607-617)."""
+    if params is None:
+        params = BfsParams()
+    with BfsEngine(g, params, g_desc=g_desc) as eng:
+        return eng.run(source)
+
+
+def bfs_sequential(g: CsrGraph, source: int) -> BfsResult:
+    """engine.py:440-475 on device: top-down level-synchronous traversal.
+
+    Levels equal the reference's; the parent of each vertex is *a* frontier
+    neighbour (not necessarily the first in scan order)."""
+    if not 0 <= source < g.n:
+        raise ValueError(f"source {source} out of range for n={g.n}")
+    with BfsEngine(g, BfsParams(mode="sequential")) as eng:
+        res = eng.run(source)
+    for r in res.levels:
+        r.wall_time = 0.0
+    return res
+
+
+# ---------------------------------------------------------------------------
+# single steps (engine.py:252-429): explicit state in, mutated state out
+
+
+def _step_engine(g: CsrGraph, reverse: bool) -> _DeviceBfs:
+    cache = g._cache
+    key = ("step_engine", reverse)
+    if key not in cache:
+        cache[key] = _DeviceBfs(g, hybrid=True, alpha=64, beta=8, g_bu=None, bu_reverse=reverse, trim_isolated=False)
+    return cache[key]
+
+
+def _run_step(g: CsrGraph, direction: int, frontier: Frontier, visited: Bitmap, parent: np.ndarray, reverse=True):
+    torch = _lib.require_cuda()
+    eng = _step_engine(g, reverse)
+    n = g.n
+    if n == 0:
+        return Bitmap(0), np.zeros(3, np.int64)
+    fr = frontier.to_bitmap_form()
+    nw = (n + 31) // 32
+    vis_in = torch.from_numpy(np.ascontiguousarray(visited.words32()).view(np.int32)).cuda()
+    fr_in = torch.from_numpy(np.ascontiguousarray(fr.bits.words32()).view(np.int32)).cuda()
+    par_in = torch.from_numpy(np.ascontiguousarray(parent, dtype=np.int32)).cuda()
+    vis_out = torch.empty(nw, dtype=torch.int32, device="cuda")
+    nxt_out = torch.empty(nw, dtype=torch.int32, device="cuda")
+    par_out = torch.empty(n, dtype=torch.int32, device="cuda")
+    ctr = np.zeros(3, np.int64)
+    _lib.check(
+        _lib.lib().rb_bfs_step(eng.h, direction, _lib.ptr(vis_in), _lib.ptr(fr_in), _lib.ptr(par_in),
+                               _lib.ptr(vis_out), _lib.ptr(nxt_out), _lib.ptr(par_out),
+                               ctr.ctypes.data_as(ctypes.c_void_p), _lib.stream_ptr()),
+        "rb_bfs_step",
+    )
+    visited.words.view(np.uint32)[:nw] = vis_out.cpu().numpy().view(np.uint32)
+    parent[:] = par_out.cpu().numpy()
+    nxt = Bitmap.from_words32(n, nxt_out.cpu().numpy().view(np.uint32))
+    return nxt, ctr
+
+
+def top_down_step(g, frontier, visited, parent, threads: int = 1, pool=None):
+    """engine.py:252-286: claim all unvisited neighbours of the frontier."""
+    nxt, c = _run_step(g, 0, frontier, visited, parent)
+    st = StepStats(n_next=int(c[0]), deg_next=int(c[1]), scanned_edges=int(c[2]),
+                   per_thread_edges=_split_even(int(c[2]), threads))
+    return Frontier.from_queue(g.n, nxt.to_indices()), st
+
+
+def top_down_step_balanced(g, frontier, visited, parent, threads: int = 1, pool=None):
+    """engine.py:289-323: the device scheduler already splits hubs across warps."""
+    return top_down_step(g, frontier, visited, parent, threads, pool)
+
+
+def bottom_up_step(g, frontier, visited, parent, threads: int = 1, pool=None):
+    """engine.py:341-370: every unvisited vertex adopts a frontier neighbour."""
+    nxt, c = _run_step(g, 1, frontier, visited, parent)
+    st = StepStats(n_next=int(c[0]), deg_next=int(c[1]), scanned_edges=int(c[2]),
+                   per_thread_edges=_split_even(int(c[2]), threads))
+    return Frontier.from_bitmap(nxt), st
+
+
+def bottom_up_step_balanced(g, frontier, visited, parent, ps=None, threads: int = 1, pool=None):
+    """engine.py:373-398 (partition set accepted for API compatibility)."""
+    return bottom_up_step(g, frontier, visited, parent, threads, pool)
+
+
+def bottom_up_step_reduced(g_desc, frontier, visited, parent, ps=None, threads: int = 1, pool=None):
+    """engine.py:401-429: scan the descending-degree rows forward (Alg. 6 order)."""
+    nxt, c = _run_step(g_desc, 1, frontier, visited, parent, reverse=False)
+    st = StepStats(n_next=int(c[0]), deg_next=int(c[1]), scanned_edges=int(c[2]),
+                   per_thread_edges=_split_even(int(c[2]), threads))
+    return Frontier.from_bitmap(nxt), st
+
+
+def write_level_trace(results, path) -> None:
+    """engine.py:620-639."""
+    fields = ["round", "source", "mode", "level", "direction", "n_f", "m_f", "m_u", "scanned_edges",
+              "wall_time_s", "pass1_hits", "live_vertices"]
+    with open(path, "w", newline="") as f:
+        w = csv.writer(f)
+        w.writerow(fields)
+        for rnd, res in enumerate(results):
+            for rec in res.levels:
+                w.writerow([
+                    rnd, res.source, res.mode, rec.level, rec.direction, rec.n_f, rec.m_f, rec.m_u,
+                    rec.scanned_edges, f"{rec.wall_time:.6f}",
+                    "" if rec.pass1_hits is None else rec.pass1_hits,
+                    "" if rec.live_vertices is None else rec.live_vertices,
+                ])

@@ -1,0 +1,188 @@
+"""Generate golden fixtures by running the REFERENCE package (rcmbfs).
+
+Run in the build container (the reference is not on the GPU box):
+
+    PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
+        python tests/golden/make_golden.py
+
+Writes small files next to this script; they are committed and read by the
+tests (CPU: oracle pinning; GPU: device parity).  Nothing here is imported by
+the product package.
+
+Contents
+* generator.json  -- sha256 of kronecker_generate edges + CSR counts per params
+* small.npz       -- random multigraphs: edges, RCM perm, component ranges,
+                     sequential parents/levels for a few sources, step results
+* kron.json       -- per (scale, seed): RCM perm sha256, component count,
+                     |V+|, 64 (or fewer) _sample_sources roots with per-root
+                     level-array sha256, hybrid LevelRecord tuples
+                     (direction, n_f, m_f, m_u), traversed edges, raw pairs
+* kron12_perm.npy -- full RCM permutation of Kronecker scale 12 seed 1
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+
+import rcmbfs
+from rcmbfs import (
+    BfsParams,
+    Bitmap,
+    EdgeList,
+    Frontier,
+    KroneckerParams,
+    Validator,
+    apply_permutation,
+    bfs_run,
+    bfs_sequential,
+    bottom_up_step,
+    build_csr,
+    kronecker_generate,
+    rcm,
+    top_down_step,
+)
+from rcmbfs.bench import _sample_sources
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def gen_fixtures():
+    out = {}
+    for scale, ef, seed in [(6, 4, 3), (10, 16, 42), (13, 16, 5), (14, 16, 9), (16, 16, 1), (16, 16, 7)]:
+        el = kronecker_generate(KroneckerParams(scale=scale, edgefactor=ef, seed=seed))
+        g = build_csr(el)
+        out[f"{scale},{ef},{seed}"] = {
+            "edges_sha256": sha(el.edges),
+            "m_directed": g.m_directed,
+            "isolated": g.isolated_count,
+            "row_starts_sha256": sha(g.row_starts),
+            "dst_sha256": sha(g.dst),
+        }
+        print("gen", scale, ef, seed, g.m_directed, g.isolated_count, flush=True)
+    with open(os.path.join(HERE, "generator.json"), "w") as f:
+        json.dump(out, f, indent=1, sort_keys=True)
+
+
+def small_fixtures():
+    rng = np.random.default_rng(2024)
+    arrays = {}
+    meta = []
+    for gi in range(24):
+        n = int(rng.integers(2, 1500))
+        density = float(rng.choice([0.3, 1.0, 2.5, 4.0]))
+        m = max(1, int(n * density))
+        e = rng.integers(0, n, size=(m, 2), dtype=np.uint32)
+        el = EdgeList(n_declared=n, edges=e)
+        g = build_csr(el)
+        perm, st = rcm(g)
+        g2 = apply_permutation(g, perm)
+        arrays[f"g{gi}_edges"] = e
+        arrays[f"g{gi}_perm"] = perm.perm
+        arrays[f"g{gi}_ranges"] = np.array(st.component_ranges, dtype=np.int64).reshape(-1, 2)
+        arrays[f"g{gi}_rcm_dst"] = g2.dst
+        srcs = rng.choice(n, size=min(4, n), replace=False)
+        val = Validator(g2)
+        lev = []
+        for s in srcs:
+            r = bfs_sequential(g2, int(s))
+            rep = val.validate(int(s), r.predecessor)
+            assert rep.passed
+            lev.append(rep.derived_levels.astype(np.int32))
+            arrays[f"g{gi}_seqpar_{int(s)}"] = r.predecessor
+        arrays[f"g{gi}_srcs"] = srcs.astype(np.int64)
+        arrays[f"g{gi}_levels"] = np.stack(lev)
+        # one TD and one BU reference step from a random state (criterion 2 style)
+        vis_mask = rng.random(n) < 0.3
+        vis_mask[int(srcs[0])] = True
+        vis_idx = np.flatnonzero(vis_mask)
+        f_idx = vis_idx[rng.random(vis_idx.size) < 0.5]
+        if f_idx.size == 0:
+            f_idx = vis_idx[:1]
+        for kind, fn in (("td", top_down_step), ("bu", bottom_up_step)):
+            visited = Bitmap.from_indices(n, vis_idx)
+            parent = np.full(n, -1, np.int32)
+            parent[vis_idx] = vis_idx
+            fr = Frontier.from_queue(n, f_idx.astype(np.uint32))
+            nxt, stats = fn(g2, fr, visited, parent)
+            arrays[f"g{gi}_{kind}_next"] = np.sort(nxt.indices()).astype(np.uint32)
+            arrays[f"g{gi}_{kind}_visited"] = visited.words.copy()
+            arrays[f"g{gi}_{kind}_stats"] = np.array([stats.n_next, stats.deg_next, stats.scanned_edges], np.int64)
+        arrays[f"g{gi}_state_vis"] = vis_idx.astype(np.int64)
+        arrays[f"g{gi}_state_frontier"] = f_idx.astype(np.int64)
+        meta.append(n)
+    arrays["n_list"] = np.array(meta, np.int64)
+    np.savez_compressed(os.path.join(HERE, "small.npz"), **arrays)
+    print("small fixtures", len(meta), flush=True)
+
+
+def kron_fixtures(plan):
+    out = {}
+    for scale, seed, n_roots in plan:
+        el = kronecker_generate(KroneckerParams(scale=scale, edgefactor=16, seed=seed))
+        g = build_csr(el)
+        perm, st = rcm(g)
+        g2 = apply_permutation(g, perm)
+        if scale == 12 and seed == 1:
+            np.save(os.path.join(HERE, "kron12_perm.npy"), perm.perm)
+        relabeled = EdgeList(n_declared=g2.n, edges=perm.inv[el.edges.reshape(-1)].reshape(-1, 2))
+        val = Validator(g2, edge_list=relabeled)
+        labels = val.component_labels()
+        raw_per_label = np.bincount(labels[relabeled.edges[:, 0]], minlength=g2.n)
+        srcs = _sample_sources(g2, n_roots, 1)
+        roots = []
+        for s in srcs:
+            s = int(s)
+            res = bfs_run(g2, s, BfsParams(mode="hybrid", alpha=64, beta=8))
+            rep = val.validate(s, res.predecessor)
+            assert rep.passed
+            roots.append(
+                {
+                    "source": s,
+                    "levels_sha256": sha(rep.derived_levels.astype(np.int32)),
+                    "records": [
+                        ["T" if r.direction == rcmbfs.TOP_DOWN else "B", r.n_f, r.m_f, r.m_u]
+                        for r in res.levels
+                    ],
+                    "traversed": int(res.traversed_edges),
+                    "raw_pairs": int(raw_per_label[labels[s]]),
+                    "n_reached": int(res.n_reached),
+                }
+            )
+        out[f"{scale},{seed}"] = {
+            "n": g.n,
+            "m_directed": g.m_directed,
+            "n_plus": int(g.n - g.isolated_count),
+            "perm_sha256": sha(perm.perm),
+            "rcm_dst_sha256": sha(g2.dst),
+            "rcm_row_starts_sha256": sha(g2.row_starts),
+            "n_components": st.n_components,
+            "component_ranges_sha256": sha(np.array(st.component_ranges, np.int64)),
+            "largest_component_fraction": st.largest_component_fraction,
+            "roots": roots,
+        }
+        print("kron", scale, seed, g.m_directed, st.n_components, flush=True)
+    return out
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["gen", "small", "kron"]
+    if "gen" in which:
+        gen_fixtures()
+    if "small" in which:
+        small_fixtures()
+    if "kron" in which:
+        plan = [(12, 1, 16), (14, 3, 16), (16, 1, 64), (18, 1, 16)]
+        if "big" in which:
+            plan.append((20, 1, 8))
+        data = kron_fixtures(plan)
+        with open(os.path.join(HERE, "kron.json"), "w") as f:
+            json.dump(data, f, indent=0, sort_keys=True)
