@@ -105,6 +105,8 @@ int rb_bfs_step(rb_bfs* h, int direction, const uint32_t* d_visited_words, const
 int32_t* rb_bfs_parent_ptr(rb_bfs* h);
 int32_t* rb_bfs_level_ptr(rb_bfs* h);
 int rb_bfs_grid(rb_bfs* h, int* blocks, int* threads);
+/* Diagnostics: average cost of one grid barrier of the traversal grid. */
+int rb_bfs_barrier_probe(rb_bfs* h, int iters, double* ns_per_barrier, void* stream);
 
 #ifdef __cplusplus
 }

@@ -47,8 +47,14 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, extra: list[str] | None = None) -> str:
+    """Compile csrc/*.cu into ``out`` (default: the in-tree library).
+
+    ``extra`` adds nvcc flags (tuning experiments build variants to a
+    separate path, e.g. ``-DRB_MINB=2``)."""
+    out = out or LIB
+    extra = list(extra or [])
+    if out == LIB and not extra and not force and not _stale():
         return LIB
     nvcc = _nvcc()
     objdir = os.path.join(PKG, "_obj")
@@ -56,25 +62,30 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     logs = []
     for src in sources():
-        obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-dc" if False else "-c", src, "-o", obj]
+        obj = os.path.join(objdir, os.path.basename(out) + "." + os.path.basename(src) + ".o")
+        cmd = [nvcc, *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         logs.append(r.stdout + r.stderr)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{r.stdout}\n{r.stderr}")
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = out + ".tmp"
     cmd = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp, *objs, "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
-    with open(os.path.join(objdir, "ptxas.log"), "w") as f:
+    os.replace(tmp, out)
+    with open(os.path.join(objdir, os.path.basename(out) + ".ptxas.log"), "w") as f:
         f.write("\n".join(logs))
     if verbose:
         print("\n".join(logs))
-    return LIB
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    args = sys.argv[1:]
+    out = None
+    if "--out" in args:
+        out = args[args.index("--out") + 1]
+    extra = [a for a in args if a.startswith("-D")]
+    print(build(force="--force" in args, verbose="-v" in args, out=out, extra=extra))

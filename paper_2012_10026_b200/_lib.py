@@ -57,6 +57,7 @@ _SIGS = {
     "rb_bfs_parent_ptr": ([P], P),
     "rb_bfs_level_ptr": ([P], P),
     "rb_bfs_grid": ([P, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+    "rb_bfs_barrier_probe": ([P, ctypes.c_int, ctypes.POINTER(ctypes.c_double), P], ctypes.c_int),
 }
 
 EXPORTED = tuple(_SIGS)
@@ -68,6 +69,9 @@ def load(path: str | None = None, build: bool = True):
     with _lock:
         if _lib is not None:
             return _lib
+        if path is None and os.environ.get("RB_LIB"):
+            path = os.environ["RB_LIB"]  # tuning variants built with _build --out
+            build = False
         if path is None:
             path = _build.LIB
             if build and os.environ.get("RB_NO_BUILD") != "1":

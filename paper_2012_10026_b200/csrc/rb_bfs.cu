@@ -3,35 +3,40 @@
 // Replaces the reference level loop BfsEngine.run (engine.py:518-604) and its
 // step kernels td_plain / td_striped / bu_range / bu_steal / bu_reduced
 // (_kernels.py:57-293).  The whole traversal of one root is ONE cooperative
-// persistent launch: levels are separated by a grid barrier, the direction
+// persistent launch: levels are separated by a grid barrier and the direction
 // policy (update_traversal_policy, engine.py:215-228) is evaluated by every
 // block from the same device counters, so no host round trip happens between
 // levels.
 //
-// State (all HBM, n_dev = non-isolated prefix of the RCM graph):
-//   vis[]          uint32 words: vertices of levels < L (plus isolated/padding)
-//   fb[3][]        frontier bitmaps, rotated: fcur = fb[L%3], fnext = fb[(L+1)%3],
-//                  fb[(L+2)%3] is zeroed during level L (it is fnext of L+1)
-//   lq[2], hq[2]   queue form of the frontier: light (deg <= kHubDeg) vertices
-//                  and hubs; hubs carry a running edge-chunk base so a hub is
-//                  split across many warps (degree-binned top-down)
+// State (HBM; n_dev = non-isolated prefix of the RCM graph):
+//   vis[]        uint32 words: vertices of levels < L (+ isolated, padding)
+//   fb[3][]      frontier bitmaps, rotated: fcur = fb[L%3], fnext = fb[(L+1)%3];
+//                fb[(L+2)%3] is zeroed during level L (it is fnext of L+1)
+//   lq[2]        light frontier vertices (deg <= kLightDeg), int32
+//   hq[2]        hub work items (chunk << 32 | v): one entry per kChunk-edge
+//                slice of a hub row, so hubs spread over many warps
 //   parent, level  int32 per vertex
-// Invariant at level L: visited = vis | fcur.  Each level ORs its own
-// frontier into vis, so no separate "publish" pass is needed.
+// Invariant: vis holds every vertex discovered so far (the current frontier
+// included), so a top-down claim is one atomicOr on vis and a bottom-up
+// step tests ~vis directly.
 //
-// Top-down: warps pull work items (32 light frontier vertices, or one
-// kHubChunk-edge slice of a hub); inside a light item the 32 rows are
-// edge-balanced with a warp prefix sum.  A neighbour is claimed with one
-// atomicOr on the next-frontier bitmap word (the visited test filters first);
-// the winner writes parent/level and appends to the next queue with a
-// warp-aggregated atomic.
-// Bottom-up: a warp owns a 1024-vertex tile (32 words).  Unvisited vertices
-// of the tile are compacted across the warp's lanes; each lane checks up to
-// kLight neighbours from the scan start (reverse row order by default: RCM ids
-// ascend with degree, so the end of a row holds the likely frontier hubs);
-// vertices still unresolved are finished by the whole warp, 32 neighbours per
-// step with ballot early exit.  The warp owns its tile's words, so visited and
-// next-frontier words are written with plain stores.
+// The path is latency-bound integer work, so both directions are written for
+// memory-level parallelism: every lane keeps several independent loads in
+// flight (unrolled edge / vertex groups), work items are sized so the whole
+// grid is busy, and there is no per-item atomic work fetching.
+//
+// Top-down: warps take items statically (light batches of 32 rows that are
+// edge-balanced with a warp prefix sum, processed 128 edges per step; or one
+// 256-edge hub slice, 8 edges per lane).  A neighbour is claimed with one
+// atomicOr on its visited word; the winner sets the next-frontier bit (RED),
+// writes parent / level and appends to the next queue (warp-aggregated).
+// Bottom-up: a warp owns kUB consecutive bitmap words (kUB*32 vertices), so
+// its visited / next-frontier words are written with plain stores.  Each lane
+// checks its unvisited vertices' rows from the scan start kK1 neighbours at a
+// time (reverse row order by default: RCM ids ascend with degree, so the end
+// of a row holds the likely frontier hubs), continuing up to kK2 checks;
+// longer rows are finished by the whole warp 256 neighbours per step with a
+// ballot early exit.
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -42,23 +47,37 @@
 
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 1024;
+#ifndef RB_MINB
+#define RB_MINB 1
+#endif
 constexpr int kWarps = kThreads / 32;
-constexpr uint32_t kHubDeg = 256;      // deg > kHubDeg -> hub queue
-constexpr uint32_t kHubChunk = 1024;   // edges per hub work item
-constexpr int kLight = 4;              // per-lane bottom-up checks before the warp takes over
-constexpr int kCountShift = 37;        // hub packing: count << 37 | chunk total
-constexpr uint64_t kChunkMask = (1ull << kCountShift) - 1;
-constexpr int64_t kRecCap = 4096;      // level records per launch
+constexpr uint32_t kLightDeg = 32;  // deg <= kLightDeg -> light queue
+constexpr int kChunkPerLane = 8;
+constexpr uint32_t kChunk = 32 * kChunkPerLane;  // edges per hub work item
+constexpr int kTdUnroll = 4;                     // light batch: edges per lane per step
+constexpr int kUB = 4;                           // bottom-up: words per warp step
+constexpr int kK1 = 2;                           // bottom-up: first-round checks per vertex
+constexpr int kK2 = 16;                          // bottom-up: per-lane checks before the warp takes over
+constexpr int kHeavyPerLane = 8;                 // warp-cooperative bottom-up: neighbours per lane per step
+constexpr int64_t kRecCap = 4096;                // level records per launch
+
+// Queue entry: a light frontier row (d <= kLightDeg) or one hub slice
+// (columns [s, s+d), d <= kChunk).  Carrying the offsets saves the dependent
+// row_starts load in the consuming level.
+struct __align__(16) QEnt {
+  long long s;
+  int32_t v;
+  int32_t d;
+};
 
 struct Slot {  // per-level counters, triple-buffered by level % 3
   unsigned long long n_next;
   unsigned long long deg_next;
   unsigned long long scanned;
-  unsigned long long lq_count;   // light queue entries for the NEXT level
-  unsigned long long hq_packed;  // hubs for the NEXT level: count << 37 | chunk total
-  unsigned long long items;      // dynamic work cursor (top-down items)
-  unsigned long long pad0, pad1;
+  unsigned long long lq_count;  // light queue entries for the NEXT level
+  unsigned long long hq_count;  // hub slices for the NEXT level
+  unsigned long long pad0, pad1, pad2;
 };
 
 struct Final {  // state after a launch (continuation for very deep graphs)
@@ -76,24 +95,26 @@ struct KParams {
   const int32_t* col_bu;
   const int32_t* deg;
   int64_t n_dev;
-  int64_t n_words;  // multiple of 32
+  int64_t n_words;  // multiple of 32 * kUB
   uint32_t* vis;
   uint32_t* fb0;
   uint32_t* fb1;
   uint32_t* fb2;
-  int32_t* lq0;
-  int32_t* lq1;
-  int32_t* hq0;
-  int32_t* hq1;
-  int64_t* hb0;
-  int64_t* hb1;
+  uint32_t* full;  // bit i: vis word i is all ones (fully visited) -- lets bottom-up skip
+  uint32_t* nz0;   // bit i: fb0 word i is nonzero -- lets the queue build skip empty words
+  uint32_t* nz1;
+  uint32_t* nz2;
+  QEnt* lq0;
+  QEnt* lq1;
+  QEnt* hq0;
+  QEnt* hq1;
   int32_t* parent;
   int32_t* level;
   Slot* slots;
   uint32_t* bar;
   rb_level_record* rec;
   Final* fin;
-  int alpha, beta, hybrid, pad_;
+  int alpha, beta, hybrid, debug;
   int64_t n_policy;
   // start state
   int64_t level0;
@@ -106,23 +127,18 @@ struct KParams {
 };
 
 __device__ __forceinline__ uint32_t* fb_of(const KParams& p, int64_t i) {
-  int64_t r = i % 3;
+  const int64_t r = i % 3;
   return r == 0 ? p.fb0 : (r == 1 ? p.fb1 : p.fb2);
 }
 
-__device__ __forceinline__ uint32_t nth_set_bit(uint32_t x, uint32_t k) {  // 0-based, LSB first
-  uint32_t pos = 0, c;
-  c = __popc(x & 0xffffu); if (k >= c) { k -= c; x >>= 16; pos += 16; }
-  c = __popc(x & 0xffu);   if (k >= c) { k -= c; x >>= 8;  pos += 8; }
-  c = __popc(x & 0xfu);    if (k >= c) { k -= c; x >>= 4;  pos += 4; }
-  c = __popc(x & 0x3u);    if (k >= c) { k -= c; x >>= 2;  pos += 2; }
-  c = x & 1u;              if (k >= c) { pos += 1; }
-  return pos;
+__device__ __forceinline__ uint32_t* nz_of(const KParams& p, int64_t i) {
+  const int64_t r = i % 3;
+  return r == 0 ? p.nz0 : (r == 1 ? p.nz1 : p.nz2);
 }
 
-__device__ __forceinline__ bool test_bit(const uint32_t* words, int32_t v) {
-  return (__ldcg(words + (v >> 5)) >> (v & 31)) & 1u;
-}
+// Frontier / visited bits: written before the last grid barrier and not
+// modified during this level (the barrier invalidates L1), so L1 may cache.
+__device__ __forceinline__ uint32_t ld_bits(const uint32_t* p) { return __ldca(p); }
 
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
@@ -130,162 +146,235 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
-// ---------------------------------------------------------------------------
-// top-down
-
-struct TdOut {
-  Slot* out;
-  int32_t* lq_out;
-  int32_t* hq_out;
-  int64_t* hb_out;
+struct Acc {
+  unsigned long long n, deg, scan;
 };
 
-// Warp-collective: every lane calls, act marks lanes with an edge (v -> w).
-__device__ __forceinline__ void td_visit(const KParams& p, int64_t L, bool act, int32_t v, int32_t w,
-                                         const uint32_t* fcur, uint32_t* fnext, const TdOut& o,
-                                         unsigned long long& my_n, unsigned long long& my_deg) {
+// Global warp index, interleaved across blocks: consecutive work items go to
+// different SMs, so a small level is not concentrated on a few SMs' LSU/L1.
+__device__ __forceinline__ uint64_t warp_slot() {
+  return (uint64_t)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+}
+
+struct TdCtx {
+  const KParams* p;
+  int64_t L;
+  const uint32_t* fcur;
+  uint32_t* fnext;
+  uint32_t* nznext;
+  Slot* out;
+};
+
+__device__ __forceinline__ QEnt ld_qent(const QEnt* q) {
+  const int4 x = __ldcg(reinterpret_cast<const int4*>(q));
+  QEnt e;
+  e.s = (long long)(((unsigned long long)(uint32_t)x.y << 32) | (uint32_t)x.x);
+  e.v = x.z;
+  e.d = x.w;
+  return e;
+}
+
+// Warp-aggregated append of frontier rows: light rows to lq, hubs as
+// kChunk-edge slices to hq.  One atomic per queue per warp (issued by two
+// lanes so they overlap).  Hub slices are written by all 32 lanes in
+// parallel, so a lane holding a huge row does not serialize the warp.
+template <int KU>
+__device__ __forceinline__ void warp_append(QEnt* lq, unsigned long long* lq_count, QEnt* hq,
+                                            unsigned long long* hq_count, const int32_t (&w)[KU],
+                                            const int64_t (&s)[KU], const uint32_t (&d)[KU], const bool (&on)[KU]) {
+  uint32_t nl = 0, nh = 0;
+  uint32_t nk[KU];
+#pragma unroll
+  for (int k = 0; k < KU; ++k) {
+    nk[k] = 0;
+    if (!on[k]) continue;
+    if (d[k] > kLightDeg) nk[k] = (d[k] + kChunk - 1) / kChunk;
+    else ++nl;
+    nh += nk[k];
+  }
+  const uint32_t il = rb::warp_incl_scan(nl);
+  const uint32_t ih = rb::warp_incl_scan(nh);
+  const uint32_t tl = __shfl_sync(RB_FULL, il, 31);
+  const uint32_t th = __shfl_sync(RB_FULL, ih, 31);
+  if ((tl | th) == 0) return;
   const uint32_t lane = rb::lane_id();
-  bool claim = false;
-  uint32_t dw = 0;
-  if (act) {
-    const int32_t wi = w >> 5;
-    const uint32_t bit = 1u << (w & 31);
-    const uint32_t seen = __ldcg(p.vis + wi) | __ldcg(fcur + wi);
-    if (!(seen & bit)) {
-      const uint32_t old = atomicOr(fnext + wi, bit);
-      if (!(old & bit)) {
-        claim = true;
-        p.parent[w] = v;
-        p.level[w] = (int32_t)(L + 1);
-        dw = (uint32_t)rb::ldg_i32(p.deg + w);
-      }
+  unsigned long long b = 0;
+  if (lane == 31 && tl) b = atomicAdd(lq_count, (unsigned long long)tl);
+  if (lane == 30 && th) b = atomicAdd(hq_count, (unsigned long long)th);
+  const unsigned long long bl = __shfl_sync(RB_FULL, b, 31);
+  const unsigned long long bh = __shfl_sync(RB_FULL, b, 30);
+  unsigned long long pl = bl + il - nl;
+#pragma unroll
+  for (int k = 0; k < KU; ++k) {
+    if (on[k] && d[k] <= kLightDeg) {
+      QEnt e;
+      e.s = s[k];
+      e.v = w[k];
+      e.d = (int32_t)d[k];
+      lq[pl++] = e;
     }
   }
-  const bool hub = claim && dw > kHubDeg;
-  if (hub) {  // rare: one 64-bit atomic reserves the slot and the chunk range
-    const unsigned long long inc =
-        (1ull << kCountShift) | (unsigned long long)((dw + kHubChunk - 1) / kHubChunk);
-    const unsigned long long old = atomicAdd(&o.out->hq_packed, inc);
-    const uint64_t slot = old >> kCountShift;
-    o.hq_out[slot] = w;
-    o.hb_out[slot] = (int64_t)(old & kChunkMask);
-  }
-  const bool light = claim && !hub;
-  const uint32_t lm = __ballot_sync(RB_FULL, light);
-  if (lm) {
-    const uint32_t leader = __ffs(lm) - 1;
-    unsigned long long base = 0;
-    if (lane == leader) base = atomicAdd(&o.out->lq_count, (unsigned long long)__popc(lm));
-    base = __shfl_sync(RB_FULL, base, leader);
-    if (light) o.lq_out[base + __popc(lm & ((1u << lane) - 1u))] = w;
-  }
-  if (claim) {
-    my_n += 1;
-    my_deg += dw;
+  for (uint32_t r = 0; r < th; r += 32) {
+    const uint32_t idx = r + lane;
+    const bool act = idx < th;
+    const uint32_t j = rb::warp_upper_bound(ih, act ? idx : th - 1);
+    uint32_t local = (act ? idx : th - 1) - (__shfl_sync(RB_FULL, ih, j) - __shfl_sync(RB_FULL, nh, j));
+    int32_t ew = 0;
+    int64_t es = 0;
+    uint32_t ed = 0;
+    bool got = false;
+#pragma unroll
+    for (int k = 0; k < KU; ++k) {
+      const uint32_t c = __shfl_sync(RB_FULL, nk[k], j);
+      const int32_t wk = __shfl_sync(RB_FULL, w[k], j);
+      const int64_t sk = rb::shfl_i64(s[k], j);
+      const uint32_t dk = __shfl_sync(RB_FULL, d[k], j);
+      if (!got && local < c) {
+        got = true;
+        ew = wk;
+        es = sk + (int64_t)local * kChunk;
+        ed = min(kChunk, dk - local * kChunk);
+      } else if (!got) {
+        local -= c;
+      }
+    }
+    if (act) {
+      QEnt e;
+      e.s = es;
+      e.v = ew;
+      e.d = (int32_t)ed;
+      hq[bh + idx] = e;
+    }
   }
 }
 
-__device__ void td_level(const KParams& p, int64_t L, const uint32_t* fcur, uint32_t* fnext,
-                         const int32_t* lq_in, const int32_t* hq_in, const int64_t* hb_in, uint64_t nl,
-                         uint64_t nh, uint64_t nchunks, const TdOut& o, unsigned long long& my_n,
-                         unsigned long long& my_deg, unsigned long long& my_scan) {
+__device__ __forceinline__ void mark_full(const KParams& p, uint64_t wi) {
+  atomicOr(p.full + (wi >> 5), 1u << (wi & 31));
+}
+
+// Warp-collective claim of KU edges per lane (v[k] -> w[k], act[k]).
+template <int KU>
+__device__ __forceinline__ void td_claim(const TdCtx& c, const int32_t (&v)[KU], const int32_t (&w)[KU],
+                                         const bool (&act)[KU], Acc& acc) {
+  const KParams& p = *c.p;
+  // claim = first to set the visited bit (vis holds every discovered vertex)
+  bool claim[KU];
+#pragma unroll
+  for (int k = 0; k < KU; ++k) {
+    claim[k] = false;
+    if (act[k]) {
+      const uint32_t bit = 1u << (w[k] & 31);
+      const uint32_t old = atomicOr(p.vis + (w[k] >> 5), bit);
+      claim[k] = !(old & bit);
+      if (claim[k] && (old | bit) == 0xffffffffu) mark_full(p, (uint64_t)(w[k] >> 5));
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < KU; ++k) {
+    if (!claim[k]) continue;
+    p.parent[w[k]] = v[k];
+    p.level[w[k]] = (int32_t)(c.L + 1);
+    const uint32_t old = atomicOr(c.fnext + (w[k] >> 5), 1u << (w[k] & 31));
+    if (old == 0u) atomicOr(c.nznext + (w[k] >> 10), 1u << ((w[k] >> 5) & 31));
+  }
+#pragma unroll
+  for (int k = 0; k < KU; ++k) {
+    if (claim[k]) {
+      acc.n += 1;
+      acc.deg += (uint32_t)rb::ldg_i32(p.deg + w[k]);
+    }
+  }
+}
+
+__device__ void td_level(const TdCtx& c, const QEnt* lq_in, const QEnt* hq_in, uint64_t nl,
+                         uint64_t nh, Acc& acc) {
+  const KParams& p = *c.p;
   const uint32_t lane = rb::lane_id();
+  const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
+  const uint64_t gw = warp_slot();
   const uint64_t nb = (nl + 31) / 32;
-  const uint64_t total = nb + nchunks;
-  while (true) {
-    unsigned long long item = 0;
-    if (lane == 0) item = atomicAdd(&o.out->items, 1ull);
-    item = __shfl_sync(RB_FULL, item, 0);
-    if (item >= total) break;
-    if (item < nb) {
-      const uint64_t idx = item * 32 + lane;
-      const bool valid = idx < nl;
+  const uint64_t total = nb + nh;
+  // hub slices first (uniform size), then light batches
+  for (uint64_t item = gw; item < total; item += nwarps) {
+    if (item < nh) {
+      const QEnt ent = ld_qent(hq_in + item);
+      const int32_t v = ent.v;
+      const int64_t a = ent.s;
+      const int64_t b = a + ent.d;
+      if (lane == 0) acc.scan += (unsigned long long)(b - a);
+      int32_t vv[kChunkPerLane], w[kChunkPerLane];
+      bool act[kChunkPerLane];
+#pragma unroll
+      for (int k = 0; k < kChunkPerLane; ++k) {
+        const int64_t j = a + lane + 32 * k;
+        act[k] = j < b;
+        vv[k] = v;
+        w[k] = act[k] ? rb::ldg_i32(p.col + j) : 0;
+      }
+      td_claim<kChunkPerLane>(c, vv, w, act, acc);
+    } else {
+      const uint64_t idx = (item - nh) * 32 + lane;
       int32_t v = 0;
       int64_t s = 0;
       uint32_t d = 0;
-      if (valid) {
-        v = __ldcg(lq_in + idx);
-        s = rb::ldg_i64(p.rs + v);
-        d = (uint32_t)(rb::ldg_i64(p.rs + v + 1) - s);
-        atomicOr(p.vis + (v >> 5), 1u << (v & 31));
+      if (idx < nl) {
+        const QEnt ent = ld_qent(lq_in + idx);
+        v = ent.v;
+        s = ent.s;
+        d = (uint32_t)ent.d;
       }
       const uint32_t incl = rb::warp_incl_scan(d);
       const uint32_t tot = __shfl_sync(RB_FULL, incl, 31);
       const uint32_t excl = incl - d;
-      my_scan += d;
-      for (uint32_t base = 0; base < tot; base += 32) {
-        const uint32_t e = base + lane;
-        const bool act = e < tot;
-        const uint32_t j = rb::warp_upper_bound(incl, act ? e : tot - 1);
-        const int32_t vj = __shfl_sync(RB_FULL, v, j);
-        const int64_t sj = rb::shfl_i64(s, j);
-        const uint32_t exj = __shfl_sync(RB_FULL, excl, j);
-        const int32_t w = act ? rb::ldg_i32(p.col + sj + (e - exj)) : 0;
-        td_visit(p, L, act, vj, w, fcur, fnext, o, my_n, my_deg);
-      }
-    } else {
-      const uint64_t c = item - nb;
-      uint64_t lo = 0, hi = nh;  // last hub whose chunk base <= c
-      while (hi - lo > 1) {
-        const uint64_t mid = (lo + hi) >> 1;
-        if ((uint64_t)__ldcg(hb_in + mid) <= c) lo = mid; else hi = mid;
-      }
-      const int32_t v = __ldcg(hq_in + lo);
-      const int64_t s = rb::ldg_i64(p.rs + v);
-      const int64_t e = rb::ldg_i64(p.rs + v + 1);
-      const uint64_t local = c - (uint64_t)__ldcg(hb_in + lo);
-      const int64_t a = s + (int64_t)(local * kHubChunk);
-      const int64_t b = min(e, a + (int64_t)kHubChunk);
-      if (local == 0 && lane == 0) atomicOr(p.vis + (v >> 5), 1u << (v & 31));
-      if (lane == 0) my_scan += (unsigned long long)(b - a);
-      for (int64_t j0 = a; j0 < b; j0 += 32) {
-        const int64_t j = j0 + lane;
-        const bool act = j < b;
-        const int32_t w = act ? rb::ldg_i32(p.col + j) : 0;
-        td_visit(p, L, act, v, w, fcur, fnext, o, my_n, my_deg);
+      acc.scan += d;
+      for (uint32_t base = 0; base < tot; base += 32 * kTdUnroll) {
+        int32_t vv[kTdUnroll], w[kTdUnroll];
+        bool act[kTdUnroll];
+#pragma unroll
+        for (int k = 0; k < kTdUnroll; ++k) {
+          const uint32_t e = base + lane + 32 * k;
+          act[k] = e < tot;
+          const uint32_t j = rb::warp_upper_bound(incl, act[k] ? e : tot - 1);
+          vv[k] = __shfl_sync(RB_FULL, v, j);
+          const int64_t sj = rb::shfl_i64(s, j);
+          const uint32_t exj = __shfl_sync(RB_FULL, excl, j);
+          w[k] = act[k] ? rb::ldg_i32(p.col + sj + (e - exj)) : 0;
+        }
+        td_claim<kTdUnroll>(c, vv, w, act, acc);
       }
     }
   }
 }
 
-// Bitmap -> queues (light / hub split) at a bottom-up -> top-down switch.
-__device__ void compact_level(const KParams& p, const uint32_t* fcur, Slot* in, int32_t* lq, int32_t* hq,
-                              int64_t* hb) {
+// Bitmap -> queues at a bottom-up -> top-down switch.  Same lane mapping as
+// the bottom-up step (lane l <-> bit l of kUB consecutive words): one degree
+// load per set bit, kUB independent loads per lane, warp-aggregated appends.
+__device__ void compact_level(const KParams& p, const uint32_t* fcur, const uint32_t* nzcur, Slot* in, QEnt* lq,
+                              QEnt* hq) {
   const uint32_t lane = rb::lane_id();
   const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
-  const uint64_t gw = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
-  const uint64_t ntiles = (uint64_t)p.n_words / 32;
-  for (uint64_t tile = gw; tile < ntiles; tile += nwarps) {
-    const uint64_t wi = tile * 32 + lane;
-    const uint32_t x = __ldcg(fcur + wi);
-    uint32_t hubmask = 0, cnt = 0;
-    for (uint32_t y = x; y; y &= y - 1) {
-      const int b = __ffs(y) - 1;
-      const int32_t v = (int32_t)(wi * 32 + b);
-      const uint32_t d = (uint32_t)rb::ldg_i32(p.deg + v);
-      if (d > kHubDeg) {
-        hubmask |= 1u << b;
-        const unsigned long long inc =
-            (1ull << kCountShift) | (unsigned long long)((d + kHubChunk - 1) / kHubChunk);
-        const unsigned long long old = atomicAdd(&in->hq_packed, inc);
-        const uint64_t slot = old >> kCountShift;
-        hq[slot] = v;
-        hb[slot] = (int64_t)(old & kChunkMask);
-      } else {
-        ++cnt;
+  const uint64_t gw = warp_slot();
+  const uint64_t nw = (uint64_t)p.n_words;
+  for (uint64_t w0 = gw * kUB; w0 < nw; w0 += nwarps * kUB) {
+    const uint32_t nzb = (ld_bits(nzcur + (w0 >> 5)) >> (w0 & 31)) & ((1u << kUB) - 1u);
+    if (!nzb) continue;  // no frontier vertex in these kUB words
+    const uint32_t x = (lane < kUB && ((nzb >> lane) & 1u)) ? __ldcg(fcur + w0 + lane) : 0u;
+    int32_t v[kUB];
+    int64_t s0[kUB];
+    uint32_t d[kUB];
+    bool on[kUB];
+#pragma unroll
+    for (int k = 0; k < kUB; ++k) {
+      on[k] = (__shfl_sync(RB_FULL, x, k) >> lane) & 1u;
+      v[k] = (int32_t)((w0 + k) * 32 + lane);
+      s0[k] = 0;
+      d[k] = 0;
+      if (on[k]) {
+        s0[k] = rb::ldg_i64(p.rs + v[k]);
+        d[k] = (uint32_t)(rb::ldg_i64(p.rs + v[k] + 1) - s0[k]);
       }
     }
-    const uint32_t incl = rb::warp_incl_scan(cnt);
-    const uint32_t tot = __shfl_sync(RB_FULL, incl, 31);
-    if (tot == 0) continue;
-    unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(&in->lq_count, (unsigned long long)tot);
-    base = __shfl_sync(RB_FULL, base, 0);
-    unsigned long long pos = base + incl - cnt;
-    for (uint32_t y = x & ~hubmask; y; y &= y - 1) {
-      const int b = __ffs(y) - 1;
-      lq[pos++] = (int32_t)(wi * 32 + b);
-    }
+    warp_append<kUB>(lq, &in->lq_count, hq, &in->hq_count, v, s0, d, on);
   }
 }
 
@@ -293,138 +382,194 @@ __device__ void compact_level(const KParams& p, const uint32_t* fcur, Slot* in, 
 // bottom-up
 
 template <bool kRev>
-__device__ void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uint32_t* fnext, uint32_t* s_found,
-                         unsigned long long& my_n, unsigned long long& my_deg, unsigned long long& my_scan) {
+__device__ __forceinline__ int64_t bu_idx(int64_t s, int64_t e, int64_t k) {
+  return kRev ? e - 1 - k : s + k;
+}
+
+template <bool kRev>
+__device__ void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uint32_t* fnext, uint32_t* nznext,
+                         Acc& acc) {
   const uint32_t lane = rb::lane_id();
   const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
-  const uint64_t gw = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
-  const uint64_t ntiles = (uint64_t)p.n_words / 32;
-  for (uint64_t tile = gw; tile < ntiles; tile += nwarps) {
-    const uint64_t wi = tile * 32 + lane;
-    const uint32_t vw = __ldcg(p.vis + wi);
-    const uint32_t fw = __ldcg(fcur + wi);
-    if (fw) p.vis[wi] = vw | fw;  // publish this level's frontier (warp owns the word)
-    const uint32_t unv = ~(vw | fw);
-    const uint32_t cnt = __popc(unv);
-    const uint32_t incl = rb::warp_incl_scan(cnt);
-    const uint32_t U = __shfl_sync(RB_FULL, incl, 31);
-    const uint32_t excl = incl - cnt;
-    s_found[lane] = 0;
-    __syncwarp();
-    for (uint32_t b0 = 0; b0 < U; b0 += 32) {
-      const uint32_t t = b0 + lane;
-      const bool act = t < U;
-      const uint32_t j = rb::warp_upper_bound(incl, act ? t : U - 1);
-      const uint32_t unvj = __shfl_sync(RB_FULL, unv, j);
-      const uint32_t exj = __shfl_sync(RB_FULL, excl, j);
-      const uint32_t bitpos = nth_set_bit(unvj, act ? t - exj : 0);
-      const int64_t v = (int64_t)(tile * 32 + j) * 32 + bitpos;
-      bool found = false, heavy = false;
-      int64_t s = 0, e = 0;
-      int32_t par = -1;
-      uint32_t checks = 0;
-      if (act) {
-        s = rb::ldg_i64(p.rs + v);
-        e = rb::ldg_i64(p.rs + v + 1);
-        const int64_t d = e - s;
-        int32_t u[kLight];
+  const uint64_t gw = warp_slot();
+  const uint64_t nw = (uint64_t)p.n_words;
+  for (uint64_t w0 = gw * kUB; w0 < nw; w0 += nwarps * kUB) {
+    // skip words that are already fully visited (fnext is pre-zeroed)
+    const uint32_t fullw = (ld_bits(p.full + (w0 >> 5)) >> (w0 & 31)) & ((1u << kUB) - 1u);
+    if (fullw == (1u << kUB) - 1u) continue;
+    const uint32_t vw = (lane < kUB && !((fullw >> lane) & 1u)) ? __ldcg(p.vis + w0 + lane) : 0xffffffffu;
+    uint32_t unv[kUB];
+    uint32_t any = 0;
 #pragma unroll
-        for (int k = 0; k < kLight; ++k)
-          u[k] = (k < d) ? rb::ldg_i32(p.col_bu + (kRev ? e - 1 - k : s + k)) : -1;
-        uint32_t hit = 0;
+    for (int k = 0; k < kUB; ++k) {
+      unv[k] = ~__shfl_sync(RB_FULL, vw, k);
+      any |= unv[k];
+    }
+    if (!any) continue;
+    // per lane: vertex v_k = (w0 + k) * 32 + lane
+    bool act[kUB], found[kUB];
+    int64_t s[kUB], e[kUB];
+    int32_t par[kUB];
+    uint32_t checks = 0;
 #pragma unroll
-        for (int k = 0; k < kLight; ++k)
-          if (u[k] >= 0 && test_bit(fcur, u[k])) hit |= 1u << k;
-        if (hit) {
-          const int k = __ffs(hit) - 1;
-          found = true;
-          par = u[k];
-          checks = k + 1;
-        } else {
-          checks = (uint32_t)(d < kLight ? d : kLight);
-          heavy = d > kLight;
+    for (int k = 0; k < kUB; ++k) {
+      act[k] = (unv[k] >> lane) & 1u;
+      found[k] = false;
+      par[k] = -1;
+      s[k] = e[k] = 0;
+      if (act[k]) {
+        const int64_t v = (int64_t)(w0 + k) * 32 + lane;
+        s[k] = rb::ldg_i64(p.rs + v);
+        e[k] = rb::ldg_i64(p.rs + v + 1);
+      }
+    }
+    // round 1: kK1 neighbours of every active vertex, all loads in flight
+    int32_t u[kUB][kK1];
+#pragma unroll
+    for (int k = 0; k < kUB; ++k)
+#pragma unroll
+      for (int t = 0; t < kK1; ++t)
+        u[k][t] = (act[k] && t < e[k] - s[k]) ? rb::ldg_i32(p.col_bu + bu_idx<kRev>(s[k], e[k], t)) : -1;
+    uint32_t hb[kUB][kK1];
+#pragma unroll
+    for (int k = 0; k < kUB; ++k)
+#pragma unroll
+      for (int t = 0; t < kK1; ++t) hb[k][t] = u[k][t] >= 0 ? ld_bits(fcur + (u[k][t] >> 5)) : 0u;
+#pragma unroll
+    for (int k = 0; k < kUB; ++k) {
+      if (!act[k]) continue;
+      const int64_t d = e[k] - s[k];
+#pragma unroll
+      for (int t = 0; t < kK1; ++t) {
+        if (!found[k] && t < d && ((hb[k][t] >> (u[k][t] & 31)) & 1u)) {
+          found[k] = true;
+          par[k] = u[k][t];
+          checks += t + 1;
         }
       }
-      uint32_t hm = __ballot_sync(RB_FULL, heavy);
-      while (hm) {  // warp-cooperative finish of long rows
+      if (!found[k]) checks += (uint32_t)(d < kK1 ? d : kK1);
+    }
+    // rounds 2..: per-lane continuation up to kK2 checks, 4 neighbours per step
+#pragma unroll
+    for (int k = 0; k < kUB; ++k) {
+      const int64_t d = e[k] - s[k];
+      const int64_t lim = d < kK2 ? d : kK2;
+      for (int64_t t0 = kK1; act[k] && !found[k] && t0 < lim; t0 += 4) {
+        int32_t uu[4];
+        uint32_t bb[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          uu[t] = (t0 + t < lim) ? rb::ldg_i32(p.col_bu + bu_idx<kRev>(s[k], e[k], t0 + t)) : -1;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) bb[t] = uu[t] >= 0 ? ld_bits(fcur + (uu[t] >> 5)) : 0u;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          if (!found[k] && uu[t] >= 0) {
+            ++checks;
+            if ((bb[t] >> (uu[t] & 31)) & 1u) {
+              found[k] = true;
+              par[k] = uu[t];
+            }
+          }
+        }
+      }
+    }
+    // heavy rows: whole warp, kHeavyPerLane * 32 neighbours per step
+#pragma unroll
+    for (int k = 0; k < kUB; ++k) {
+      uint32_t hm = __ballot_sync(RB_FULL, act[k] && !found[k] && (e[k] - s[k]) > kK2);
+      while (hm) {
         const int h = __ffs(hm) - 1;
         hm &= hm - 1;
-        const int64_t hs = rb::shfl_i64(s, h);
-        const int64_t he = rb::shfl_i64(e, h);
-        const int64_t len = he - hs - kLight;
+        const int64_t hs = rb::shfl_i64(s[k], h);
+        const int64_t he = rb::shfl_i64(e[k], h);
+        const int64_t len = he - hs;
         int32_t hpar = -1;
-        int64_t hchecks = len;
-        for (int64_t r = 0; r < len; r += 32) {
-          const int64_t k = r + lane;
-          bool hit = false;
-          int32_t uu = 0;
-          if (k < len) {
-            uu = rb::ldg_i32(p.col_bu + (kRev ? he - kLight - 1 - k : hs + kLight + k));
-            hit = test_bit(fcur, uu);
+        int64_t hchecks = len - kK2;
+        for (int64_t r = kK2; r < len; r += 32 * kHeavyPerLane) {
+          int32_t uu[kHeavyPerLane];
+          uint32_t bb[kHeavyPerLane];
+#pragma unroll
+          for (int t = 0; t < kHeavyPerLane; ++t) {
+            const int64_t q = r + lane * kHeavyPerLane + t;  // lane-major: scan order preserved per lane
+            uu[t] = q < len ? rb::ldg_i32(p.col_bu + bu_idx<kRev>(hs, he, q)) : -1;
           }
-          const uint32_t hb = __ballot_sync(RB_FULL, hit);
-          if (hb) {
-            const int f = __ffs(hb) - 1;
-            hpar = __shfl_sync(RB_FULL, uu, f);
-            hchecks = r + f + 1;
+#pragma unroll
+          for (int t = 0; t < kHeavyPerLane; ++t) bb[t] = uu[t] >= 0 ? ld_bits(fcur + (uu[t] >> 5)) : 0u;
+          int first = -1;
+          int32_t fu = -1;
+#pragma unroll
+          for (int t = kHeavyPerLane - 1; t >= 0; --t)
+            if (uu[t] >= 0 && ((bb[t] >> (uu[t] & 31)) & 1u)) {
+              first = t;
+              fu = uu[t];
+            }
+          const uint32_t hit = __ballot_sync(RB_FULL, first >= 0);
+          if (hit) {
+            const int f = __ffs(hit) - 1;  // lowest lane = earliest in scan order
+            const int ft = __shfl_sync(RB_FULL, first, f);
+            hpar = __shfl_sync(RB_FULL, fu, f);
+            hchecks = (r - kK2) + f * kHeavyPerLane + ft + 1;
             break;
           }
         }
         if ((int)lane == h) {
           checks += (uint32_t)hchecks;
           if (hpar >= 0) {
-            found = true;
-            par = hpar;
+            found[k] = true;
+            par[k] = hpar;
           }
         }
       }
-      if (found) {
-        p.parent[v] = par;
-        p.level[v] = (int32_t)(L + 1);
-        atomicOr(s_found + j, 1u << bitpos);
-        my_n += 1;
-        my_deg += (unsigned long long)(e - s);
-      }
-      my_scan += checks;
     }
-    __syncwarp();
-    fnext[wi] = s_found[lane];  // full-word store: also clears stale bits
-    __syncwarp();
+    // results: parents, levels, next-frontier words (fnext is pre-zeroed)
+    uint32_t nzmask = 0;
+#pragma unroll
+    for (int k = 0; k < kUB; ++k) {
+      if (found[k]) {
+        const int64_t v = (int64_t)(w0 + k) * 32 + lane;
+        p.parent[v] = par[k];
+        p.level[v] = (int32_t)(L + 1);
+        acc.n += 1;
+        acc.deg += (unsigned long long)(e[k] - s[k]);
+      }
+      const uint32_t fm = __ballot_sync(RB_FULL, found[k]);
+      nzmask |= (fm != 0u) << k;
+      if (lane == (uint32_t)k && fm) {
+        fnext[w0 + k] = fm;
+        const uint32_t nv = ~unv[k] | fm;
+        p.vis[w0 + k] = nv;  // the warp owns these words
+        if (nv == 0xffffffffu) mark_full(p, w0 + k);
+      }
+    }
+    if (lane == 0 && nzmask) atomicOr(nznext + (w0 >> 5), nzmask << (w0 & 31));
+    acc.scan += checks;
   }
 }
 
 // ---------------------------------------------------------------------------
 
-__device__ __forceinline__ void block_add3(unsigned long long* red, unsigned long long a, unsigned long long b,
-                                           unsigned long long c, Slot* out) {
-  a = rb::warp_sum_u64(a);
-  b = rb::warp_sum_u64(b);
-  c = rb::warp_sum_u64(c);
+__device__ __forceinline__ void block_add3(unsigned long long* red, const Acc& a, Slot* out) {
+  const unsigned long long A = rb::warp_sum_u64(a.n);
+  const unsigned long long B = rb::warp_sum_u64(a.deg);
+  const unsigned long long C = rb::warp_sum_u64(a.scan);
   const uint32_t w = threadIdx.x >> 5;
   if (rb::lane_id() == 0) {
-    red[w * 3 + 0] = a;
-    red[w * 3 + 1] = b;
-    red[w * 3 + 2] = c;
+    red[w * 3 + 0] = A;
+    red[w * 3 + 1] = B;
+    red[w * 3 + 2] = C;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long A = 0, B = 0, C = 0;
-    for (int i = 0; i < kWarps; ++i) {
-      A += red[i * 3];
-      B += red[i * 3 + 1];
-      C += red[i * 3 + 2];
-    }
-    if (A) atomicAdd(&out->n_next, A);
-    if (B) atomicAdd(&out->deg_next, B);
-    if (C) atomicAdd(&out->scanned, C);
+  if (threadIdx.x < 3) {
+    unsigned long long s = 0;
+    for (int i = 0; i < kWarps; ++i) s += red[i * 3 + threadIdx.x];
+    if (s) atomicAdd(threadIdx.x == 0 ? &out->n_next : (threadIdx.x == 1 ? &out->deg_next : &out->scanned), s);
   }
 }
 
 template <bool kRev>
-__global__ void __launch_bounds__(kThreads) bfs_persistent(KParams p) {
-  __shared__ uint32_t s_found_all[kWarps][32];
+__global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
   __shared__ unsigned long long s_red[kWarps * 3];
-  uint32_t* s_found = s_found_all[threadIdx.x >> 5];
   const uint32_t nblocks = gridDim.x;
   const uint64_t gtid = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
   const uint64_t gthreads = (uint64_t)nblocks * kThreads;
@@ -438,6 +583,7 @@ __global__ void __launch_bounds__(kThreads) bfs_persistent(KParams p) {
     mu = p.m_directed - mf;
   }
   int64_t done = 0;
+  uint32_t epoch = 0;
   uint64_t t_prev = 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) t_prev = globaltimer();
 
@@ -447,34 +593,35 @@ __global__ void __launch_bounds__(kThreads) bfs_persistent(KParams p) {
     const uint32_t* fcur = fb_of(p, L);
     uint32_t* fnext = fb_of(p, L + 1);
     uint32_t* fzero = fb_of(p, L + 2);
-    // zero ahead: next level's fnext bitmap and the counter slot of level L+1
-    for (uint64_t i = gtid; i < (uint64_t)p.n_words; i += gthreads) fzero[i] = 0u;
+    uint32_t* nzzero = nz_of(p, L + 2);
+    // zero ahead: next level's fnext bitmap (+ summary) and the counter slot of level L+1
+    for (uint64_t i = gtid; i < (uint64_t)p.n_words / 4; i += gthreads)
+      reinterpret_cast<uint4*>(fzero)[i] = make_uint4(0u, 0u, 0u, 0u);
+    for (uint64_t i = gtid; i < (uint64_t)p.n_words / 32; i += gthreads) nzzero[i] = 0u;
     if (blockIdx.x == 0 && threadIdx.x < sizeof(Slot) / 8)
       reinterpret_cast<unsigned long long*>(p.slots + ((L + 1) % 3))[threadIdx.x] = 0ull;
 
-    unsigned long long my_n = 0, my_deg = 0, my_scan = 0;
+    Acc acc{0, 0, 0};
     if (dir == 0) {
-      int32_t* lq_in = (L & 1) ? p.lq1 : p.lq0;
-      int32_t* hq_in = (L & 1) ? p.hq1 : p.hq0;
-      int64_t* hb_in = (L & 1) ? p.hb1 : p.hb0;
+      QEnt* lq_in = (L & 1) ? p.lq1 : p.lq0;
+      QEnt* hq_in = (L & 1) ? p.hq1 : p.hq0;
       if (need_compact) {
-        compact_level(p, fcur, in, lq_in, hq_in, hb_in);
-        rb::grid_barrier(p.bar, nblocks);
+        compact_level(p, fcur, nz_of(p, L), in, lq_in, hq_in);
+        rb::grid_barrier(p.bar, nblocks, epoch);
       }
-      const uint64_t nl = rb::ld_relaxed_u64(&in->lq_count);
-      const uint64_t hp = rb::ld_relaxed_u64(&in->hq_packed);
-      TdOut o;
-      o.out = out;
-      o.lq_out = (L & 1) ? p.lq0 : p.lq1;
-      o.hq_out = (L & 1) ? p.hq0 : p.hq1;
-      o.hb_out = (L & 1) ? p.hb0 : p.hb1;
-      td_level(p, L, fcur, fnext, lq_in, hq_in, hb_in, nl, hp >> kCountShift, hp & kChunkMask, o, my_n,
-               my_deg, my_scan);
+      TdCtx c;
+      c.p = &p;
+      c.L = L;
+      c.fcur = fcur;
+      c.fnext = fnext;
+      c.nznext = nz_of(p, L + 1);
+      c.out = out;
+      td_level(c, lq_in, hq_in, rb::ld_relaxed_u64(&in->lq_count), rb::ld_relaxed_u64(&in->hq_count), acc);
     } else {
-      bu_level<kRev>(p, L, fcur, fnext, s_found, my_n, my_deg, my_scan);
+      bu_level<kRev>(p, L, fcur, fnext, nz_of(p, L + 1), acc);
     }
-    block_add3(s_red, my_n, my_deg, my_scan, out);
-    rb::grid_barrier(p.bar, nblocks);
+    block_add3(s_red, acc, out);
+    rb::grid_barrier(p.bar, nblocks, epoch);
 
     const int64_t n_next = (int64_t)rb::ld_relaxed_u64(&out->n_next);
     const int64_t deg_next = (int64_t)rb::ld_relaxed_u64(&out->deg_next);
@@ -503,7 +650,7 @@ __global__ void __launch_bounds__(kThreads) bfs_persistent(KParams p) {
       else
         ndir = ((double)nf < (double)p.n_policy / (double)p.beta) ? 0 : 1;
     }
-    need_compact = (dir == 1 && ndir == 0);
+    need_compact = ndir == 0;  // queues are always rebuilt from the frontier bitmap
     dir = ndir;
     ++L;
     ++done;
@@ -525,16 +672,54 @@ __global__ void bfs_seed(KParams p, int64_t src) {
   p.parent[src] = (int32_t)src;
   p.level[src] = 0;
   p.fb0[src >> 5] |= 1u << (src & 31);
-  const int64_t d = p.rs[src + 1] - p.rs[src];
+  p.nz0[src >> 10] |= 1u << ((src >> 5) & 31);
+  p.vis[src >> 5] |= 1u << (src & 31);
+  if (p.vis[src >> 5] == 0xffffffffu) p.full[src >> 10] |= 1u << ((src >> 5) & 31);
+  const int64_t s0 = p.rs[src];
+  const uint32_t d = (uint32_t)(p.rs[src + 1] - s0);
   Slot* in = p.slots + 2;  // inputs of level 0 = outputs of "level -1"
-  if (d > (int64_t)kHubDeg) {
-    p.hq0[0] = (int32_t)src;
-    p.hb0[0] = 0;
-    in->hq_packed = (1ull << kCountShift) | (unsigned long long)((d + kHubChunk - 1) / kHubChunk);
+  if (d > kLightDeg) {
+    uint32_t c = 0;
+    for (; c * kChunk < d; ++c) {
+      QEnt e;
+      e.s = s0 + (long long)c * kChunk;
+      e.v = (int32_t)src;
+      e.d = (int32_t)min(kChunk, d - c * kChunk);
+      p.hq0[c] = e;
+    }
+    in->hq_count = c;
   } else {
-    p.lq0[0] = (int32_t)src;
+    QEnt e;
+    e.s = s0;
+    e.v = (int32_t)src;
+    e.d = (int32_t)d;
+    p.lq0[0] = e;
     in->lq_count = 1;
   }
+}
+
+// nz[j] bit i <=> words[32*j + i] != 0
+__global__ void make_nz(const uint32_t* words, uint32_t* nz, int64_t n_nz) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_nz; j += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t f = 0;
+    for (int i = 0; i < 32; ++i) f |= (words[j * 32 + i] != 0u ? 1u : 0u) << i;
+    nz[j] = f;
+  }
+}
+
+// full[j] bit i <=> vis word 32*j + i is all ones
+__global__ void make_full(const uint32_t* vis, uint32_t* full, int64_t n_full) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_full; j += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t f = 0;
+    for (int i = 0; i < 32; ++i) f |= (vis[j * 32 + i] == 0xffffffffu ? 1u : 0u) << i;
+    full[j] = f;
+  }
+}
+
+// Diagnostics: cost of the grid barrier alone (same grid as the traversal).
+__global__ void __launch_bounds__(kThreads, 1) barrier_probe(uint32_t* bar, int iters) {
+  uint32_t epoch = 0;
+  for (int i = 0; i < iters; ++i) rb::grid_barrier(bar, gridDim.x, epoch);
 }
 
 __global__ void words_or3(const uint32_t* a, const uint32_t* b, const uint32_t* c, uint32_t* out, int64_t n,
@@ -569,13 +754,16 @@ struct rb_bfs {
   rb_bfs_params prm;
   int64_t n_dev;
   int64_t n_words;
-  uint32_t* vis_template;  // isolated + padding premarked
-  uint32_t* pad_mask;      // padding bits only
+  uint32_t* vis_template;   // isolated + padding premarked
+  uint32_t* full_template;  // summary of vis_template
+  uint32_t* pad_mask;       // padding bits only
+  int64_t n_full;
   int blocks;
   int sms;
   int bu_reverse;
   int64_t source;
   std::vector<rb_level_record> recs;
+  int64_t levels_per_launch;  // kRecCap; RB_LEVELS_PER_LAUNCH=1 gives one launch per level (profiling)
   bool launched;
   void* stream;
 };
@@ -604,9 +792,16 @@ extern "C" int rb_bfs_create(const int64_t* d_row_starts, const int32_t* d_col, 
   memset(&h->kp, 0, sizeof(h->kp));
   h->prm = *params;
   h->n_dev = n_dev;
-  h->n_words = ((n_dev + 1023) / 1024) * 32;
+  const int64_t tile = 32 * 32 * kUB;  // vertex alignment of the word arrays
+  h->n_words = ((n_dev + tile - 1) / tile) * (tile / 32);
   h->bu_reverse = params->bu_reverse;
   h->launched = false;
+  h->levels_per_launch = kRecCap;
+  if (const char* env = getenv("RB_DEBUG")) h->kp.debug = atoi(env);
+  if (const char* env = getenv("RB_LEVELS_PER_LAUNCH")) {
+    const long long v = atoll(env);
+    if (v >= 1 && v <= kRecCap) h->levels_per_launch = v;
+  }
   KParams& k = h->kp;
   k.rs = d_row_starts;
   k.col = d_col;
@@ -615,8 +810,10 @@ extern "C" int rb_bfs_create(const int64_t* d_row_starts, const int32_t* d_col, 
   k.n_dev = n_dev;
   k.n_words = h->n_words;
   const size_t wb = (size_t)h->n_words * 4;
+  // hub-slice queue capacity: sum over vertices of ceil(deg / kChunk)
+  const size_t nhub = (size_t)n_dev + (size_t)(params->m_directed / kChunk) + 64;
   int rc = RB_OK;
-#define RB_ALLOC(ptr, bytes)                               \
+#define RB_ALLOC(ptr, bytes) \
   if (rc == RB_OK) rc = alloc_dev((void**)&(ptr), (bytes));
   RB_ALLOC(k.vis, wb);
   RB_ALLOC(k.fb0, wb);
@@ -624,13 +821,16 @@ extern "C" int rb_bfs_create(const int64_t* d_row_starts, const int32_t* d_col, 
   RB_ALLOC(k.fb2, wb);
   RB_ALLOC(h->vis_template, wb);
   RB_ALLOC(h->pad_mask, wb);
-  RB_ALLOC(k.lq0, (size_t)n_dev * 4);
-  RB_ALLOC(k.lq1, (size_t)n_dev * 4);
-  const size_t nhub = (size_t)n_dev + 2;
-  RB_ALLOC(k.hq0, nhub * 4);
-  RB_ALLOC(k.hq1, nhub * 4);
-  RB_ALLOC(k.hb0, nhub * 8);
-  RB_ALLOC(k.hb1, nhub * 8);
+  h->n_full = h->n_words / 32;
+  RB_ALLOC(k.full, (size_t)h->n_full * 4);
+  RB_ALLOC(k.nz0, (size_t)h->n_full * 4);
+  RB_ALLOC(k.nz1, (size_t)h->n_full * 4);
+  RB_ALLOC(k.nz2, (size_t)h->n_full * 4);
+  RB_ALLOC(h->full_template, (size_t)h->n_full * 4);
+  RB_ALLOC(k.lq0, (size_t)n_dev * sizeof(QEnt));
+  RB_ALLOC(k.lq1, (size_t)n_dev * sizeof(QEnt));
+  RB_ALLOC(k.hq0, nhub * sizeof(QEnt));
+  RB_ALLOC(k.hq1, nhub * sizeof(QEnt));
   RB_ALLOC(k.parent, (size_t)n_dev * 4);
   RB_ALLOC(k.level, (size_t)n_dev * 4);
   RB_ALLOC(k.slots, 3 * sizeof(Slot));
@@ -654,6 +854,7 @@ extern "C" int rb_bfs_create(const int64_t* d_row_starts, const int32_t* d_col, 
     return RB_ERR_CUDA;
   }
   if (d_isolated_words) words_or<<<256, 256>>>(h->vis_template, d_isolated_words, (n_dev + 31) / 32);
+  make_full<<<256, 256>>>(h->vis_template, h->full_template, h->n_full);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     rb_set_error("rb_bfs_create: %s", cudaGetErrorString(e));
@@ -684,7 +885,7 @@ extern "C" int rb_bfs_destroy(rb_bfs* h) {
   if (!h) return RB_OK;
   KParams& k = h->kp;
   void* ptrs[] = {k.vis, k.fb0, k.fb1, k.fb2, h->vis_template, h->pad_mask, k.lq0, k.lq1, k.hq0, k.hq1,
-                  k.hb0, k.hb1, k.parent, k.level, k.slots, k.bar, k.rec, k.fin};
+                  k.parent, k.level, k.slots, k.bar, k.rec, k.fin, k.full, h->full_template, k.nz0, k.nz1, k.nz2};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete h;
@@ -707,6 +908,8 @@ static int reset_common(rb_bfs* h, cudaStream_t s) {
   RB_CUDA_TRY(cudaMemsetAsync(k.level, 0xff, (size_t)h->n_dev * 4, s));
   RB_CUDA_TRY(cudaMemsetAsync(k.fb0, 0, wb, s));
   RB_CUDA_TRY(cudaMemsetAsync(k.fb1, 0, wb, s));
+  RB_CUDA_TRY(cudaMemsetAsync(k.nz0, 0, (size_t)h->n_full * 4, s));
+  RB_CUDA_TRY(cudaMemsetAsync(k.nz1, 0, (size_t)h->n_full * 4, s));
   RB_CUDA_TRY(cudaMemsetAsync(k.slots, 0, 3 * sizeof(Slot), s));
   RB_CUDA_TRY(cudaMemsetAsync(k.bar, 0, 64, s));
   return RB_OK;
@@ -722,6 +925,7 @@ extern "C" int rb_bfs_reset(rb_bfs* h, int64_t source, void* stream) {
   int rc = reset_common(h, s);
   if (rc) return rc;
   RB_CUDA_TRY(cudaMemcpyAsync(h->kp.vis, h->vis_template, (size_t)h->n_words * 4, cudaMemcpyDeviceToDevice, s));
+  RB_CUDA_TRY(cudaMemcpyAsync(h->kp.full, h->full_template, (size_t)h->n_full * 4, cudaMemcpyDeviceToDevice, s));
   bfs_seed<<<1, 32, 0, s>>>(h->kp, source);
   RB_CUDA_TRY(cudaGetLastError());
   h->source = source;
@@ -758,7 +962,7 @@ extern "C" int rb_bfs_traverse(rb_bfs* h, void* stream) {
   if (!h) return RB_ERR_ARG;
   h->launched = true;
   h->stream = stream;
-  return launch(h, (cudaStream_t)stream, 0, 0, 0, kRecCap, 1, -1, 0);
+  return launch(h, (cudaStream_t)stream, 0, 0, 0, h->levels_per_launch, 1, -1, 0);
 }
 
 extern "C" int rb_bfs_results(rb_bfs* h, int32_t* parent_out, int32_t* level_out, rb_level_record* h_records,
@@ -773,14 +977,14 @@ extern "C" int rb_bfs_results(rb_bfs* h, int32_t* parent_out, int32_t* level_out
       RB_CUDA_TRY(cudaStreamSynchronize(s));
       size_t old = h->recs.size();
       h->recs.resize(old + (size_t)f.levels_done);
-      if (f.levels_done)
-      {
+      if (f.levels_done) {
         RB_CUDA_TRY(cudaMemcpyAsync(h->recs.data() + old, h->kp.rec,
                                     (size_t)f.levels_done * sizeof(rb_level_record), cudaMemcpyDeviceToHost, s));
         RB_CUDA_TRY(cudaStreamSynchronize(s));
       }
       if (f.nf <= 0) break;
-      int rc = launch(h, s, f.L, f.dir, f.need_compact, kRecCap, f.nf, f.mf, f.mu);
+      RB_CUDA_TRY(cudaMemsetAsync(h->kp.bar, 0, 64, s));
+      int rc = launch(h, s, f.L, f.dir, f.need_compact, h->levels_per_launch, f.nf, f.mf, f.mu);
       if (rc) return rc;
     }
     h->launched = false;
@@ -813,8 +1017,12 @@ extern "C" int rb_bfs_step(rb_bfs* h, int direction, const uint32_t* d_visited_w
   if (rc) return rc;
   RB_CUDA_TRY(cudaMemcpyAsync(k.vis, h->pad_mask, (size_t)h->n_words * 4, cudaMemcpyDeviceToDevice, s));
   words_or<<<256, 256, 0, s>>>(k.vis, d_visited_words, nw_in);
+  words_or<<<256, 256, 0, s>>>(k.vis, d_frontier_words, nw_in);
+  make_full<<<256, 256, 0, s>>>(k.vis, k.full, h->n_full);
   RB_CUDA_TRY(cudaMemcpyAsync(k.fb0, d_frontier_words, (size_t)nw_in * 4, cudaMemcpyDeviceToDevice, s));
+  make_nz<<<256, 256, 0, s>>>(k.fb0, k.nz0, h->n_full);
   RB_CUDA_TRY(cudaMemcpyAsync(k.parent, d_parent_in, (size_t)h->n_dev * 4, cudaMemcpyDeviceToDevice, s));
+  h->source = 0;
   rc = launch(h, s, 0, direction, direction == 0 ? 1 : 0, 1, 1, 0, 0);
   if (rc) return rc;
   words_or3<<<256, 256, 0, s>>>(k.vis, k.fb0, k.fb1, d_visited_out, nw_in, h->pad_mask);
@@ -828,5 +1036,27 @@ extern "C" int rb_bfs_step(rb_bfs* h, int direction, const uint32_t* d_visited_w
     h_counters[1] = (int64_t)sl.deg_next;
     h_counters[2] = (int64_t)sl.scanned;
   }
+  return RB_OK;
+}
+
+extern "C" int rb_bfs_barrier_probe(rb_bfs* h, int iters, double* ns_per_barrier, void* stream) {
+  if (!h || iters <= 0) return RB_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  RB_CUDA_TRY(cudaMemsetAsync(h->kp.bar, 0, 64, s));
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  uint32_t* bar = h->kp.bar;
+  void* args[] = {&bar, &iters};
+  RB_CUDA_TRY(cudaEventRecord(a, s));
+  RB_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)barrier_probe, dim3(h->blocks), dim3(kThreads), args, 0, s));
+  RB_CUDA_TRY(cudaEventRecord(b, s));
+  RB_CUDA_TRY(cudaEventSynchronize(b));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  RB_CUDA_TRY(cudaMemsetAsync(h->kp.bar, 0, 64, s));
+  *ns_per_barrier = 1e6 * (double)ms / iters;
   return RB_OK;
 }

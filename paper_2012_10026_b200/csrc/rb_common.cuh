@@ -29,23 +29,24 @@ __device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
 __device__ __forceinline__ int32_t ldg_i32(const int32_t* p) { return __ldg(p); }
 __device__ __forceinline__ int64_t ldg_i64(const int64_t* p) { return __ldg(p); }
 
-// Grid-wide barrier for a cooperative (co-resident) launch.  bar[0] = arrival
-// count, bar[1] = generation.  Release/acquire at gpu scope orders every
-// block's global writes before any block proceeds.
-__device__ __forceinline__ void grid_barrier(uint32_t* bar, uint32_t nblocks) {
+// Grid-wide barrier for a cooperative (co-resident) launch.  bar[0] is a
+// monotonically increasing arrival counter (zeroed before the launch); the
+// e-th barrier of a launch completes when it reaches e * nblocks.  One
+// fire-and-forget release add per block, a relaxed spin, one acquire fence --
+// no counter reset, no generation word.
+__device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void grid_barrier(uint32_t* bar, uint32_t nblocks, uint32_t& epoch) {
+  ++epoch;
   __syncthreads();
   if (threadIdx.x == 0) {
-    uint32_t gen = ld_acquire_u32(bar + 1);
-    __threadfence();
-    uint32_t arrived = atomicAdd(bar, 1u);
-    if (arrived == nblocks - 1) {
-      atomicExch(bar, 0u);
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      while (ld_acquire_u32(bar + 1) == gen) __nanosleep(32);
+    red_release_add(bar, 1u);
+    const uint32_t target = epoch * nblocks;
+    while ((int32_t)(ld_relaxed_u32(bar) - target) < 0) {
     }
-    __threadfence();
+    __threadfence();  // acquire side (also invalidates this SM's L1)
   }
   __syncthreads();
 }
