@@ -100,7 +100,6 @@ struct KParams {
   uint32_t* fb0;
   uint32_t* fb1;
   uint32_t* fb2;
-  uint32_t* full;  // bit i: vis word i is all ones (fully visited) -- lets bottom-up skip
   uint32_t* nz0;   // bit i: fb0 word i is nonzero -- lets the queue build skip empty words
   uint32_t* nz1;
   uint32_t* nz2;
@@ -248,9 +247,6 @@ __device__ __forceinline__ void warp_append(QEnt* lq, unsigned long long* lq_cou
   }
 }
 
-__device__ __forceinline__ void mark_full(const KParams& p, uint64_t wi) {
-  atomicOr(p.full + (wi >> 5), 1u << (wi & 31));
-}
 
 // Warp-collective claim of KU edges per lane (v[k] -> w[k], act[k]).
 template <int KU>
@@ -266,7 +262,6 @@ __device__ __forceinline__ void td_claim(const TdCtx& c, const int32_t (&v)[KU],
       const uint32_t bit = 1u << (w[k] & 31);
       const uint32_t old = atomicOr(p.vis + (w[k] >> 5), bit);
       claim[k] = !(old & bit);
-      if (claim[k] && (old | bit) == 0xffffffffu) mark_full(p, (uint64_t)(w[k] >> 5));
     }
   }
 #pragma unroll
@@ -393,11 +388,14 @@ __device__ void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uint
   const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
   const uint64_t gw = warp_slot();
   const uint64_t nw = (uint64_t)p.n_words;
-  for (uint64_t w0 = gw * kUB; w0 < nw; w0 += nwarps * kUB) {
-    // skip words that are already fully visited (fnext is pre-zeroed)
-    const uint32_t fullw = (ld_bits(p.full + (w0 >> 5)) >> (w0 & 31)) & ((1u << kUB) - 1u);
-    if (fullw == (1u << kUB) - 1u) continue;
-    const uint32_t vw = (lane < kUB && !((fullw >> lane) & 1u)) ? __ldcg(p.vis + w0 + lane) : 0xffffffffu;
+  const uint64_t stride = nwarps * kUB;
+  // software pipeline: the visited words of the next step are in flight while
+  // this step works (fnext is pre-zeroed, so fully visited words need no store)
+  uint64_t w0 = gw * kUB;
+  uint32_t vw_next = (w0 < nw && lane < kUB) ? __ldcg(p.vis + w0 + lane) : 0xffffffffu;
+  for (; w0 < nw; w0 += stride) {
+    const uint32_t vw = vw_next;
+    vw_next = (w0 + stride < nw && lane < kUB) ? __ldcg(p.vis + w0 + stride + lane) : 0xffffffffu;
     uint32_t unv[kUB];
     uint32_t any = 0;
 #pragma unroll
@@ -539,7 +537,6 @@ __device__ void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uint
         fnext[w0 + k] = fm;
         const uint32_t nv = ~unv[k] | fm;
         p.vis[w0 + k] = nv;  // the warp owns these words
-        if (nv == 0xffffffffu) mark_full(p, w0 + k);
       }
     }
     if (lane == 0 && nzmask) atomicOr(nznext + (w0 >> 5), nzmask << (w0 & 31));
@@ -674,7 +671,6 @@ __global__ void bfs_seed(KParams p, int64_t src) {
   p.fb0[src >> 5] |= 1u << (src & 31);
   p.nz0[src >> 10] |= 1u << ((src >> 5) & 31);
   p.vis[src >> 5] |= 1u << (src & 31);
-  if (p.vis[src >> 5] == 0xffffffffu) p.full[src >> 10] |= 1u << ((src >> 5) & 31);
   const int64_t s0 = p.rs[src];
   const uint32_t d = (uint32_t)(p.rs[src + 1] - s0);
   Slot* in = p.slots + 2;  // inputs of level 0 = outputs of "level -1"
@@ -704,15 +700,6 @@ __global__ void make_nz(const uint32_t* words, uint32_t* nz, int64_t n_nz) {
     uint32_t f = 0;
     for (int i = 0; i < 32; ++i) f |= (words[j * 32 + i] != 0u ? 1u : 0u) << i;
     nz[j] = f;
-  }
-}
-
-// full[j] bit i <=> vis word 32*j + i is all ones
-__global__ void make_full(const uint32_t* vis, uint32_t* full, int64_t n_full) {
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_full; j += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t f = 0;
-    for (int i = 0; i < 32; ++i) f |= (vis[j * 32 + i] == 0xffffffffu ? 1u : 0u) << i;
-    full[j] = f;
   }
 }
 
@@ -755,9 +742,8 @@ struct rb_bfs {
   int64_t n_dev;
   int64_t n_words;
   uint32_t* vis_template;   // isolated + padding premarked
-  uint32_t* full_template;  // summary of vis_template
   uint32_t* pad_mask;       // padding bits only
-  int64_t n_full;
+  int64_t n_full;  // words of a nonzero-summary bitmap (n_words / 32)
   int blocks;
   int sms;
   int bu_reverse;
@@ -822,11 +808,9 @@ extern "C" int rb_bfs_create(const int64_t* d_row_starts, const int32_t* d_col, 
   RB_ALLOC(h->vis_template, wb);
   RB_ALLOC(h->pad_mask, wb);
   h->n_full = h->n_words / 32;
-  RB_ALLOC(k.full, (size_t)h->n_full * 4);
   RB_ALLOC(k.nz0, (size_t)h->n_full * 4);
   RB_ALLOC(k.nz1, (size_t)h->n_full * 4);
   RB_ALLOC(k.nz2, (size_t)h->n_full * 4);
-  RB_ALLOC(h->full_template, (size_t)h->n_full * 4);
   RB_ALLOC(k.lq0, (size_t)n_dev * sizeof(QEnt));
   RB_ALLOC(k.lq1, (size_t)n_dev * sizeof(QEnt));
   RB_ALLOC(k.hq0, nhub * sizeof(QEnt));
@@ -854,7 +838,6 @@ extern "C" int rb_bfs_create(const int64_t* d_row_starts, const int32_t* d_col, 
     return RB_ERR_CUDA;
   }
   if (d_isolated_words) words_or<<<256, 256>>>(h->vis_template, d_isolated_words, (n_dev + 31) / 32);
-  make_full<<<256, 256>>>(h->vis_template, h->full_template, h->n_full);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     rb_set_error("rb_bfs_create: %s", cudaGetErrorString(e));
@@ -885,7 +868,7 @@ extern "C" int rb_bfs_destroy(rb_bfs* h) {
   if (!h) return RB_OK;
   KParams& k = h->kp;
   void* ptrs[] = {k.vis, k.fb0, k.fb1, k.fb2, h->vis_template, h->pad_mask, k.lq0, k.lq1, k.hq0, k.hq1,
-                  k.parent, k.level, k.slots, k.bar, k.rec, k.fin, k.full, h->full_template, k.nz0, k.nz1, k.nz2};
+                  k.parent, k.level, k.slots, k.bar, k.rec, k.fin, k.nz0, k.nz1, k.nz2};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete h;
@@ -925,7 +908,6 @@ extern "C" int rb_bfs_reset(rb_bfs* h, int64_t source, void* stream) {
   int rc = reset_common(h, s);
   if (rc) return rc;
   RB_CUDA_TRY(cudaMemcpyAsync(h->kp.vis, h->vis_template, (size_t)h->n_words * 4, cudaMemcpyDeviceToDevice, s));
-  RB_CUDA_TRY(cudaMemcpyAsync(h->kp.full, h->full_template, (size_t)h->n_full * 4, cudaMemcpyDeviceToDevice, s));
   bfs_seed<<<1, 32, 0, s>>>(h->kp, source);
   RB_CUDA_TRY(cudaGetLastError());
   h->source = source;
@@ -1018,7 +1000,6 @@ extern "C" int rb_bfs_step(rb_bfs* h, int direction, const uint32_t* d_visited_w
   RB_CUDA_TRY(cudaMemcpyAsync(k.vis, h->pad_mask, (size_t)h->n_words * 4, cudaMemcpyDeviceToDevice, s));
   words_or<<<256, 256, 0, s>>>(k.vis, d_visited_words, nw_in);
   words_or<<<256, 256, 0, s>>>(k.vis, d_frontier_words, nw_in);
-  make_full<<<256, 256, 0, s>>>(k.vis, k.full, h->n_full);
   RB_CUDA_TRY(cudaMemcpyAsync(k.fb0, d_frontier_words, (size_t)nw_in * 4, cudaMemcpyDeviceToDevice, s));
   make_nz<<<256, 256, 0, s>>>(k.fb0, k.nz0, h->n_full);
   RB_CUDA_TRY(cudaMemcpyAsync(k.parent, d_parent_in, (size_t)h->n_dev * 4, cudaMemcpyDeviceToDevice, s));
