@@ -24,6 +24,12 @@ enum { RB_OK = 0, RB_ERR_ARG = 1, RB_ERR_CUDA = 2, RB_ERR_NCCL = 3, RB_ERR_OOM =
 const char* rb_last_error(void);
 int rb_version(void);
 
+/* ---- input: replaces generator.py:114-148 (kronecker_generate) ---------- */
+/* Writes n*edgefactor (u,v) uint32 pairs, byte-identical with the reference
+ * (numpy Philox4x64-10 streams keyed (seed, chunk), 65,536-edge chunks). */
+int rb_kronecker_generate(int scale, int64_t edgefactor, uint64_t seed, double a, double b, double c,
+                          uint32_t* d_edges, void* stream);
+
 /* ---- CSR build: replaces graph.py:85-120 (build_csr) -------------------- */
 /* Stage 1 (sizes + error check).  d_edges: m_raw (u,v) uint32 pairs.
  * On an out-of-range edge returns RB_ERR_ARG with *bad_index = first index.

@@ -40,6 +40,8 @@ class BfsParamsC(ctypes.Structure):
 _SIGS = {
     "rb_last_error": ([], ctypes.c_char_p),
     "rb_version": ([], ctypes.c_int),
+    "rb_kronecker_generate": ([ctypes.c_int, I64, ctypes.c_uint64, ctypes.c_double, ctypes.c_double,
+                               ctypes.c_double, P, P], ctypes.c_int),
     "rb_csr_workspace_bytes": ([I64, I64], SZ),
     "rb_csr_build": ([P, I64, I64, P, SZ, ctypes.POINTER(I64), ctypes.POINTER(I64), P], ctypes.c_int),
     "rb_csr_emit": ([P, I64, I64, P, P, P, P], ctypes.c_int),

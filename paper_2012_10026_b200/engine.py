@@ -230,6 +230,7 @@ class _DeviceBfs:
             "rb_bfs_create",
         )
         self.pinned = torch.empty(n_dev, dtype=torch.int32, pin_memory=True)
+        self._recs = (_lib.LevelRecordC * 256)()
         self.ev0 = torch.cuda.Event(enable_timing=True)
         self.ev1 = torch.cuda.Event(enable_timing=True)
 
@@ -253,20 +254,28 @@ class _DeviceBfs:
         _lib.check(L.rb_bfs_traverse(self.h, s), "rb_bfs_traverse")
         self.ev1.record()
 
-    def results(self, want_parent=True, want_level=False, level_out=None):
+    def results(self, want_parent=True, level_out=None, parent_host=None):
+        """Drain the traversal; copy parents (to ``parent_host`` numpy int32
+        array if given, else the pinned buffer) and return (records, seconds)."""
         L = _lib.lib()
-        cap = 1 << 16
-        recs = (_lib.LevelRecordC * cap)()
         nrec = ctypes.c_int64(0)
-        lvl = level_out
+        if parent_host is not None:
+            pdst = ctypes.c_void_p(parent_host.ctypes.data)
+        elif want_parent:
+            pdst = _lib.ptr(self.pinned)
+        else:
+            pdst = None
         _lib.check(
-            L.rb_bfs_results(self.h, _lib.ptr(self.pinned) if want_parent else None,
-                             _lib.ptr(lvl) if lvl is not None else None, recs, cap, ctypes.byref(nrec),
-                             _lib.stream_ptr()),
+            L.rb_bfs_results(self.h, pdst, _lib.ptr(level_out) if level_out is not None else None, self._recs,
+                             len(self._recs), ctypes.byref(nrec), _lib.stream_ptr()),
             "rb_bfs_results",
         )
+        if nrec.value > len(self._recs):  # very deep traversal: records are kept host-side until reset
+            self._recs = (_lib.LevelRecordC * nrec.value)()
+            _lib.check(L.rb_bfs_results(self.h, None, None, self._recs, len(self._recs), ctypes.byref(nrec),
+                                        _lib.stream_ptr()), "rb_bfs_results")
         elapsed = self.ev0.elapsed_time(self.ev1) / 1000.0
-        return recs[: min(nrec.value, cap)], elapsed
+        return self._recs[: nrec.value], elapsed
 
     def level_tensor(self):
         """Device int32 level array over [0, n_dev) (valid after results())."""
@@ -343,9 +352,9 @@ class BfsEngine:
         if source >= self._dev.n_dev or int(self._deg_dev[source].item()) == 0:
             return self._trivial(source)
         self._dev.traverse(source)
-        recs, elapsed = self._dev.results()
-        pred = np.full(g.n, -1, dtype=np.int32)
-        pred[: self._dev.n_dev] = self._dev.pinned.numpy()
+        pred = np.empty(g.n, dtype=np.int32)
+        recs, elapsed = self._dev.results(parent_host=pred)  # D2H straight into the result array
+        pred[self._dev.n_dev :] = -1  # dropped isolated tail
         levels = _records_to_levels(recs)
         traversed = sum(r.m_f for r in levels) // 2  # = sum deg[reached] // 2 (engine.py:599-600)
         return BfsResult(source=source, n=g.n, predecessor=pred, levels=levels, elapsed_time=elapsed,
