@@ -56,9 +56,10 @@ constexpr uint32_t kLightDeg = 32;  // deg <= kLightDeg -> light queue
 constexpr int kChunkPerLane = 8;
 constexpr uint32_t kChunk = 32 * kChunkPerLane;  // edges per hub work item
 constexpr int kTdUnroll = 4;                     // light batch: edges per lane per step
-constexpr int kUB = 4;                           // bottom-up: words per warp step
+constexpr int kUB = 4;                           // compaction: words per warp step
+constexpr int kBU = 8;                           // bottom-up: words per warp step
 constexpr int kK1 = 2;                           // bottom-up: first-round checks per vertex
-constexpr int kK2 = 16;                          // bottom-up: per-lane checks before the warp takes over
+constexpr int kK2 = 10;                          // bottom-up: per-lane checks before the warp takes over
 constexpr int kHeavyPerLane = 8;                 // warp-cooperative bottom-up: neighbours per lane per step
 constexpr int64_t kRecCap = 4096;                // level records per launch
 
@@ -94,6 +95,7 @@ struct KParams {
   const int32_t* col;
   const int32_t* col_bu;
   const int32_t* deg;
+  const int2* hot;  // per vertex: the first two neighbours in bottom-up scan order (-1 = none)
   int64_t n_dev;
   int64_t n_words;  // multiple of 32 * kUB
   uint32_t* vis;
@@ -381,164 +383,193 @@ __device__ __forceinline__ int64_t bu_idx(int64_t s, int64_t e, int64_t k) {
   return kRev ? e - 1 - k : s + k;
 }
 
+// Warp-cooperative finish of one long row (rank h of the warp): checks
+// [t0, d) in scan order, kHeavyPerLane * 32 neighbours per step, ballot
+// early exit.  Returns the parent (or -1); *checks gets the checks done.
+template <bool kRev>
+__device__ __forceinline__ int32_t bu_heavy(const KParams& p, const uint32_t* fcur, int64_t hs, int64_t he,
+                                            int64_t t0, int64_t* checks) {
+  const uint32_t lane = rb::lane_id();
+  const int64_t len = he - hs;
+  for (int64_t r = t0; r < len; r += 32 * kHeavyPerLane) {
+    int32_t uu[kHeavyPerLane];
+    uint32_t bb[kHeavyPerLane];
+#pragma unroll
+    for (int t = 0; t < kHeavyPerLane; ++t) {
+      const int64_t q = r + lane * kHeavyPerLane + t;  // lane-major: scan order preserved per lane
+      uu[t] = q < len ? rb::ldg_i32(p.col_bu + bu_idx<kRev>(hs, he, q)) : -1;
+    }
+#pragma unroll
+    for (int t = 0; t < kHeavyPerLane; ++t) bb[t] = uu[t] >= 0 ? ld_bits(fcur + (uu[t] >> 5)) : 0u;
+    int first = -1;
+    int32_t fu = -1;
+#pragma unroll
+    for (int t = kHeavyPerLane - 1; t >= 0; --t)
+      if (uu[t] >= 0 && ((bb[t] >> (uu[t] & 31)) & 1u)) {
+        first = t;
+        fu = uu[t];
+      }
+    const uint32_t hit = __ballot_sync(RB_FULL, first >= 0);
+    if (hit) {
+      const int f = __ffs(hit) - 1;  // lowest lane = earliest in scan order
+      const int ft = __shfl_sync(RB_FULL, first, f);
+      *checks = (r - t0) + f * kHeavyPerLane + ft + 1;
+      return __shfl_sync(RB_FULL, fu, f);
+    }
+  }
+  *checks = len - t0;
+  return -1;
+}
+
 template <bool kRev>
 __device__ void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uint32_t* fnext, uint32_t* nznext,
-                         Acc& acc) {
+                         Acc& acc, uint32_t* s_found, uint32_t* s_pair) {
   const uint32_t lane = rb::lane_id();
   const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
   const uint64_t gw = warp_slot();
   const uint64_t nw = (uint64_t)p.n_words;
-  const uint64_t stride = nwarps * kUB;
+  const uint64_t stride = nwarps * kBU;
   // software pipeline: the visited words of the next step are in flight while
   // this step works (fnext is pre-zeroed, so fully visited words need no store)
-  uint64_t w0 = gw * kUB;
-  uint32_t vw_next = (w0 < nw && lane < kUB) ? __ldcg(p.vis + w0 + lane) : 0xffffffffu;
+  uint64_t w0 = gw * kBU;
+  uint32_t vw_next = (w0 < nw && lane < kBU) ? __ldcg(p.vis + w0 + lane) : 0xffffffffu;
   for (; w0 < nw; w0 += stride) {
     const uint32_t vw = vw_next;
-    vw_next = (w0 + stride < nw && lane < kUB) ? __ldcg(p.vis + w0 + stride + lane) : 0xffffffffu;
-    uint32_t unv[kUB];
-    uint32_t any = 0;
+    vw_next = (w0 + stride < nw && lane < kBU) ? __ldcg(p.vis + w0 + stride + lane) : 0xffffffffu;
+    // lane l owns vertex (w0 + k) * 32 + l of each of the kBU words
+    uint32_t actm = 0;
 #pragma unroll
-    for (int k = 0; k < kUB; ++k) {
-      unv[k] = ~__shfl_sync(RB_FULL, vw, k);
-      any |= unv[k];
-    }
-    if (!any) continue;
-    // per lane: vertex v_k = (w0 + k) * 32 + lane
-    bool act[kUB], found[kUB];
-    int64_t s[kUB], e[kUB];
-    int32_t par[kUB];
-    uint32_t checks = 0;
+    for (int k = 0; k < kBU; ++k) actm |= ((~__shfl_sync(RB_FULL, vw, k) >> lane) & 1u) << k;
+    if (!__any_sync(RB_FULL, actm != 0)) continue;
+    const int64_t vbase = (int64_t)w0 * 32 + lane;
+    // round 1: the two scan-first neighbours from the compact `hot` side
+    // array (8 B per vertex, coalesced) -- all kBU loads in flight
+    int2 hv[kBU];
+    uint32_t dg[kBU];
 #pragma unroll
-    for (int k = 0; k < kUB; ++k) {
-      act[k] = (unv[k] >> lane) & 1u;
-      found[k] = false;
-      par[k] = -1;
-      s[k] = e[k] = 0;
-      if (act[k]) {
-        const int64_t v = (int64_t)(w0 + k) * 32 + lane;
-        s[k] = rb::ldg_i64(p.rs + v);
-        e[k] = rb::ldg_i64(p.rs + v + 1);
+    for (int k = 0; k < kBU; ++k) {
+      hv[k] = make_int2(-1, -1);
+      dg[k] = 0;
+      if ((actm >> k) & 1u) {
+        hv[k] = __ldg(p.hot + vbase + 32 * k);
+        dg[k] = (uint32_t)rb::ldg_i32(p.deg + vbase + 32 * k);
       }
     }
-    // round 1: kK1 neighbours of every active vertex, all loads in flight
-    int32_t u[kUB][kK1];
+    uint32_t hb0[kBU], hb1[kBU];
 #pragma unroll
-    for (int k = 0; k < kUB; ++k)
-#pragma unroll
-      for (int t = 0; t < kK1; ++t)
-        u[k][t] = (act[k] && t < e[k] - s[k]) ? rb::ldg_i32(p.col_bu + bu_idx<kRev>(s[k], e[k], t)) : -1;
-    uint32_t hb[kUB][kK1];
-#pragma unroll
-    for (int k = 0; k < kUB; ++k)
-#pragma unroll
-      for (int t = 0; t < kK1; ++t) hb[k][t] = u[k][t] >= 0 ? ld_bits(fcur + (u[k][t] >> 5)) : 0u;
-#pragma unroll
-    for (int k = 0; k < kUB; ++k) {
-      if (!act[k]) continue;
-      const int64_t d = e[k] - s[k];
-#pragma unroll
-      for (int t = 0; t < kK1; ++t) {
-        if (!found[k] && t < d && ((hb[k][t] >> (u[k][t] & 31)) & 1u)) {
-          found[k] = true;
-          par[k] = u[k][t];
-          checks += t + 1;
-        }
-      }
-      if (!found[k]) checks += (uint32_t)(d < kK1 ? d : kK1);
+    for (int k = 0; k < kBU; ++k) {
+      hb0[k] = hv[k].x >= 0 ? ld_bits(fcur + (hv[k].x >> 5)) : 0u;
+      hb1[k] = hv[k].y >= 0 ? ld_bits(fcur + (hv[k].y >> 5)) : 0u;
     }
-    // rounds 2..: per-lane continuation up to kK2 checks, 4 neighbours per step
+    uint32_t foundm = 0, needm = 0, checks = 0;
 #pragma unroll
-    for (int k = 0; k < kUB; ++k) {
-      const int64_t d = e[k] - s[k];
-      const int64_t lim = d < kK2 ? d : kK2;
-      for (int64_t t0 = kK1; act[k] && !found[k] && t0 < lim; t0 += 4) {
-        int32_t uu[4];
-        uint32_t bb[4];
+    for (int k = 0; k < kBU; ++k) {
+      if (!((actm >> k) & 1u)) continue;
+      int32_t par = -1;
+      if (hv[k].x >= 0 && ((hb0[k] >> (hv[k].x & 31)) & 1u)) {
+        par = hv[k].x;
+        checks += 1;
+      } else if (hv[k].y >= 0 && ((hb1[k] >> (hv[k].y & 31)) & 1u)) {
+        par = hv[k].y;
+        checks += 2;
+      } else {
+        checks += dg[k] < 2u ? dg[k] : 2u;
+        if (dg[k] > 2u) needm |= 1u << k;
+      }
+      if (par >= 0) {
+        foundm |= 1u << k;
+        p.parent[vbase + 32 * k] = par;
+        p.level[vbase + 32 * k] = (int32_t)(L + 1);
+        acc.n += 1;
+        acc.deg += dg[k];
+      }
+    }
+    // Longer rows that did not hit: the (lane, k) pairs are compacted across
+    // the warp through shared memory so every lane continues one row (up to
+    // kK2 checks, 4 per step); rows longer still are finished by the whole warp.
+    uint32_t* fm_s = s_found;  // kBU words: found bits per word
 #pragma unroll
-        for (int t = 0; t < 4; ++t)
-          uu[t] = (t0 + t < lim) ? rb::ldg_i32(p.col_bu + bu_idx<kRev>(s[k], e[k], t0 + t)) : -1;
+    for (int k = 0; k < kBU; ++k) {
+      const uint32_t fm = __ballot_sync(RB_FULL, (foundm >> k) & 1u);
+      if (lane == 0) fm_s[k] = fm;
+    }
+    const uint32_t np = __popc(needm);
+    const uint32_t incl = rb::warp_incl_scan(np);
+    const uint32_t npairs = __shfl_sync(RB_FULL, incl, 31);
+    if (npairs) {
+      uint32_t pos = incl - np;
+      for (uint32_t m = needm; m; m &= m - 1) {
+        const uint32_t k = __ffs(m) - 1;
+        s_pair[pos] = (min(dg[k], 0xffffffu) << 8) | (k << 5) | lane;  // degree saturates at 2^24-1
+        ++pos;
+      }
+      __syncwarp();
+      for (uint32_t base = 0; base < npairs; base += 32) {
+        const bool mine = base + lane < npairs;
+        uint32_t idx = 0, d = 0;
+        int64_t s0 = 0;
+        int32_t par = -1;
+        if (mine) {
+          const uint32_t ent = s_pair[base + lane];
+          idx = ent & 0xffu;
+          d = ent >> 8;
+          if (d == 0xffffffu) d = (uint32_t)rb::ldg_i32(p.deg + (int64_t)w0 * 32 + idx);
+          s0 = rb::ldg_i64(p.rs + (int64_t)w0 * 32 + idx);
+          const int64_t e0 = s0 + d;
+          const int64_t lim = d < (uint32_t)kK2 ? d : kK2;
+          for (int64_t t0 = 2; par < 0 && t0 < lim; t0 += 4) {
+            int32_t uu[4];
+            uint32_t bb[4];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) bb[t] = uu[t] >= 0 ? ld_bits(fcur + (uu[t] >> 5)) : 0u;
+            for (int t = 0; t < 4; ++t)
+              uu[t] = (t0 + t < lim) ? rb::ldg_i32(p.col_bu + bu_idx<kRev>(s0, e0, t0 + t)) : -1;
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          if (!found[k] && uu[t] >= 0) {
-            ++checks;
-            if ((bb[t] >> (uu[t] & 31)) & 1u) {
-              found[k] = true;
-              par[k] = uu[t];
+            for (int t = 0; t < 4; ++t) bb[t] = uu[t] >= 0 ? ld_bits(fcur + (uu[t] >> 5)) : 0u;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              if (par < 0 && uu[t] >= 0) {
+                ++checks;
+                if ((bb[t] >> (uu[t] & 31)) & 1u) par = uu[t];
+              }
             }
           }
         }
-      }
-    }
-    // heavy rows: whole warp, kHeavyPerLane * 32 neighbours per step
-#pragma unroll
-    for (int k = 0; k < kUB; ++k) {
-      uint32_t hm = __ballot_sync(RB_FULL, act[k] && !found[k] && (e[k] - s[k]) > kK2);
-      while (hm) {
-        const int h = __ffs(hm) - 1;
-        hm &= hm - 1;
-        const int64_t hs = rb::shfl_i64(s[k], h);
-        const int64_t he = rb::shfl_i64(e[k], h);
-        const int64_t len = he - hs;
-        int32_t hpar = -1;
-        int64_t hchecks = len - kK2;
-        for (int64_t r = kK2; r < len; r += 32 * kHeavyPerLane) {
-          int32_t uu[kHeavyPerLane];
-          uint32_t bb[kHeavyPerLane];
-#pragma unroll
-          for (int t = 0; t < kHeavyPerLane; ++t) {
-            const int64_t q = r + lane * kHeavyPerLane + t;  // lane-major: scan order preserved per lane
-            uu[t] = q < len ? rb::ldg_i32(p.col_bu + bu_idx<kRev>(hs, he, q)) : -1;
-          }
-#pragma unroll
-          for (int t = 0; t < kHeavyPerLane; ++t) bb[t] = uu[t] >= 0 ? ld_bits(fcur + (uu[t] >> 5)) : 0u;
-          int first = -1;
-          int32_t fu = -1;
-#pragma unroll
-          for (int t = kHeavyPerLane - 1; t >= 0; --t)
-            if (uu[t] >= 0 && ((bb[t] >> (uu[t] & 31)) & 1u)) {
-              first = t;
-              fu = uu[t];
-            }
-          const uint32_t hit = __ballot_sync(RB_FULL, first >= 0);
-          if (hit) {
-            const int f = __ffs(hit) - 1;  // lowest lane = earliest in scan order
-            const int ft = __shfl_sync(RB_FULL, first, f);
-            hpar = __shfl_sync(RB_FULL, fu, f);
-            hchecks = (r - kK2) + f * kHeavyPerLane + ft + 1;
-            break;
+        uint32_t hm = __ballot_sync(RB_FULL, mine && par < 0 && d > (uint32_t)kK2);
+        while (hm) {
+          const int h = __ffs(hm) - 1;
+          hm &= hm - 1;
+          const int64_t hs = rb::shfl_i64(s0, h);
+          const int64_t he = hs + __shfl_sync(RB_FULL, d, h);
+          int64_t hc = 0;
+          const int32_t hp = bu_heavy<kRev>(p, fcur, hs, he, kK2, &hc);
+          if ((int)lane == h) {
+            checks += (uint32_t)hc;
+            par = hp;
           }
         }
-        if ((int)lane == h) {
-          checks += (uint32_t)hchecks;
-          if (hpar >= 0) {
-            found[k] = true;
-            par[k] = hpar;
-          }
+        if (mine && par >= 0) {
+          const int64_t v = (int64_t)w0 * 32 + idx;
+          p.parent[v] = par;
+          p.level[v] = (int32_t)(L + 1);
+          acc.n += 1;
+          acc.deg += d;
+          atomicOr(fm_s + (idx >> 5), 1u << (idx & 31));
         }
       }
+      __syncwarp();
     }
-    // results: parents, levels, next-frontier words (fnext is pre-zeroed)
+    // next-frontier words (pre-zeroed) and visited words: the warp owns them
     uint32_t nzmask = 0;
 #pragma unroll
-    for (int k = 0; k < kUB; ++k) {
-      if (found[k]) {
-        const int64_t v = (int64_t)(w0 + k) * 32 + lane;
-        p.parent[v] = par[k];
-        p.level[v] = (int32_t)(L + 1);
-        acc.n += 1;
-        acc.deg += (unsigned long long)(e[k] - s[k]);
-      }
-      const uint32_t fm = __ballot_sync(RB_FULL, found[k]);
+    for (int k = 0; k < kBU; ++k) {
+      const uint32_t fm = fm_s[k];
       nzmask |= (fm != 0u) << k;
       if (lane == (uint32_t)k && fm) {
         fnext[w0 + k] = fm;
-        const uint32_t nv = ~unv[k] | fm;
-        p.vis[w0 + k] = nv;  // the warp owns these words
+        p.vis[w0 + k] = vw | fm;
       }
     }
+    __syncwarp();
     if (lane == 0 && nzmask) atomicOr(nznext + (w0 >> 5), nzmask << (w0 & 31));
     acc.scan += checks;
   }
@@ -567,6 +598,8 @@ __device__ __forceinline__ void block_add3(unsigned long long* red, const Acc& a
 template <bool kRev>
 __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
   __shared__ unsigned long long s_red[kWarps * 3];
+  __shared__ uint32_t s_bu_found[kWarps][kBU];
+  __shared__ uint32_t s_bu_pair[kWarps][32 * kBU];
   const uint32_t nblocks = gridDim.x;
   const uint64_t gtid = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
   const uint64_t gthreads = (uint64_t)nblocks * kThreads;
@@ -615,7 +648,8 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
       c.out = out;
       td_level(c, lq_in, hq_in, rb::ld_relaxed_u64(&in->lq_count), rb::ld_relaxed_u64(&in->hq_count), acc);
     } else {
-      bu_level<kRev>(p, L, fcur, fnext, nz_of(p, L + 1), acc);
+      const uint32_t wib = threadIdx.x >> 5;
+      bu_level<kRev>(p, L, fcur, fnext, nz_of(p, L + 1), acc, s_bu_found[wib], s_bu_pair[wib]);
     }
     block_add3(s_red, acc, out);
     rb::grid_barrier(p.bar, nblocks, epoch);
@@ -694,6 +728,18 @@ __global__ void bfs_seed(KParams p, int64_t src) {
   }
 }
 
+// hot[v] = the first two neighbours of v in bottom-up scan order (-1 if absent)
+__global__ void make_hot(const int64_t* rs, const int32_t* col, int64_t n, int reverse, int2* hot) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = rs[v], e = rs[v + 1];
+    const int64_t d = e - s;
+    int2 h = make_int2(-1, -1);
+    if (d > 0) h.x = reverse ? col[e - 1] : col[s];
+    if (d > 1) h.y = reverse ? col[e - 2] : col[s + 1];
+    hot[v] = h;
+  }
+}
+
 // nz[j] bit i <=> words[32*j + i] != 0
 __global__ void make_nz(const uint32_t* words, uint32_t* nz, int64_t n_nz) {
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_nz; j += (int64_t)gridDim.x * blockDim.x) {
@@ -743,6 +789,7 @@ struct rb_bfs {
   int64_t n_words;
   uint32_t* vis_template;   // isolated + padding premarked
   uint32_t* pad_mask;       // padding bits only
+  int2* hot;
   int64_t n_full;  // words of a nonzero-summary bitmap (n_words / 32)
   int blocks;
   int sms;
@@ -778,7 +825,7 @@ extern "C" int rb_bfs_create(const int64_t* d_row_starts, const int32_t* d_col, 
   memset(&h->kp, 0, sizeof(h->kp));
   h->prm = *params;
   h->n_dev = n_dev;
-  const int64_t tile = 32 * 32 * kUB;  // vertex alignment of the word arrays
+  const int64_t tile = 32 * 32 * kBU;  // vertex alignment of the word arrays
   h->n_words = ((n_dev + tile - 1) / tile) * (tile / 32);
   h->bu_reverse = params->bu_reverse;
   h->launched = false;
@@ -816,6 +863,7 @@ extern "C" int rb_bfs_create(const int64_t* d_row_starts, const int32_t* d_col, 
   RB_ALLOC(k.hq0, nhub * sizeof(QEnt));
   RB_ALLOC(k.hq1, nhub * sizeof(QEnt));
   RB_ALLOC(k.parent, (size_t)n_dev * 4);
+  RB_ALLOC(h->hot, (size_t)n_dev * sizeof(int2));
   RB_ALLOC(k.level, (size_t)n_dev * 4);
   RB_ALLOC(k.slots, 3 * sizeof(Slot));
   RB_ALLOC(k.bar, 64);
@@ -832,6 +880,8 @@ extern "C" int rb_bfs_create(const int64_t* d_row_starts, const int32_t* d_col, 
   k.n_policy = params->n_policy;
 
   make_pad_mask<<<256, 256>>>(h->pad_mask, n_dev, h->n_words);
+  make_hot<<<1024, 256>>>(d_row_starts, k.col_bu, n_dev, params->bu_reverse, h->hot);
+  k.hot = h->hot;
   if (cudaMemcpy(h->vis_template, h->pad_mask, wb, cudaMemcpyDeviceToDevice) != cudaSuccess) {
     rb_set_error("rb_bfs_create: template copy failed");
     rb_bfs_destroy(h);
@@ -868,7 +918,7 @@ extern "C" int rb_bfs_destroy(rb_bfs* h) {
   if (!h) return RB_OK;
   KParams& k = h->kp;
   void* ptrs[] = {k.vis, k.fb0, k.fb1, k.fb2, h->vis_template, h->pad_mask, k.lq0, k.lq1, k.hq0, k.hq1,
-                  k.parent, k.level, k.slots, k.bar, k.rec, k.fin, k.nz0, k.nz1, k.nz2};
+                  k.parent, k.level, k.slots, k.bar, k.rec, k.fin, k.nz0, k.nz1, k.nz2, h->hot};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete h;
