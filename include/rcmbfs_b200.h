@@ -77,6 +77,8 @@ typedef struct {
   int64_t scanned_edges; /* TD: edges examined; BU: neighbour checks */
   int64_t t_ns;          /* device %globaltimer duration of the level */
   int64_t n_next;
+  int64_t t_queue_ns;    /* part of t_ns spent rebuilding the top-down queues */
+  int64_t reserved;
 } rb_level_record;
 
 typedef struct {

@@ -26,7 +26,7 @@ SZ = ctypes.c_size_t
 class LevelRecordC(ctypes.Structure):
     _fields_ = [
         ("level", I64), ("direction", I64), ("n_f", I64), ("m_f", I64), ("m_u", I64),
-        ("scanned_edges", I64), ("t_ns", I64), ("n_next", I64),
+        ("scanned_edges", I64), ("t_ns", I64), ("n_next", I64), ("t_queue_ns", I64), ("reserved", I64),
     ]
 
 

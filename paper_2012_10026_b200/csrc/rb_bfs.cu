@@ -53,6 +53,8 @@ constexpr int kThreads = 1024;
 #endif
 constexpr int kWarps = kThreads / 32;
 constexpr uint32_t kLightDeg = 32;  // deg <= kLightDeg -> light queue
+constexpr uint32_t kTinyDeg = 2;    // deg <= kTinyDeg -> tiny queue (neighbours inline)
+constexpr int kTinyPerLane = 4;     // tiny rows per lane per top-down item
 constexpr int kChunkPerLane = 8;
 constexpr uint32_t kChunk = 32 * kChunkPerLane;  // edges per hub work item
 constexpr int kTdUnroll = 4;                     // light batch: edges per lane per step
@@ -72,13 +74,20 @@ struct __align__(16) QEnt {
   int32_t d;
 };
 
+struct __align__(32) VInfo {  // top-down row record (see ld_vinfo)
+  long long s;
+  int32_t d;
+  int32_t n0;
+  int32_t n1;
+  int32_t pad[3];
+};
+
 struct Slot {  // per-level counters, triple-buffered by level % 3
   unsigned long long n_next;
   unsigned long long deg_next;
   unsigned long long scanned;
-  unsigned long long lq_count;  // light queue entries for the NEXT level
-  unsigned long long hq_count;  // hub slices for the NEXT level
-  unsigned long long pad0, pad1, pad2;
+  unsigned long long hq_count;  // hub slices appended by phase A of the NEXT level
+  unsigned long long pad0, pad1, pad2, pad3;
 };
 
 struct Final {  // state after a launch (continuation for very deep graphs)
@@ -105,9 +114,8 @@ struct KParams {
   uint32_t* nz0;   // bit i: fb0 word i is nonzero -- lets the queue build skip empty words
   uint32_t* nz1;
   uint32_t* nz2;
-  QEnt* lq0;
-  QEnt* lq1;
-  QEnt* hq0;
+  const VInfo* vinfo;  // top-down row records
+  QEnt* hq0;           // hub slices of the current top-down level (alternating)
   QEnt* hq1;
   int32_t* parent;
   int32_t* level;
@@ -163,7 +171,6 @@ struct TdCtx {
   const uint32_t* fcur;
   uint32_t* fnext;
   uint32_t* nznext;
-  Slot* out;
 };
 
 __device__ __forceinline__ QEnt ld_qent(const QEnt* q) {
@@ -175,93 +182,44 @@ __device__ __forceinline__ QEnt ld_qent(const QEnt* q) {
   return e;
 }
 
-// Warp-aggregated append of frontier rows: light rows to lq, hubs as
-// kChunk-edge slices to hq.  One atomic per queue per warp (issued by two
-// lanes so they overlap).  Hub slices are written by all 32 lanes in
-// parallel, so a lane holding a huge row does not serialize the warp.
-template <int KU>
-__device__ __forceinline__ void warp_append(QEnt* lq, unsigned long long* lq_count, QEnt* hq,
-                                            unsigned long long* hq_count, const int32_t (&w)[KU],
-                                            const int64_t (&s)[KU], const uint32_t (&d)[KU], const bool (&on)[KU]) {
-  uint32_t nl = 0, nh = 0;
-  uint32_t nk[KU];
-#pragma unroll
-  for (int k = 0; k < KU; ++k) {
-    nk[k] = 0;
-    if (!on[k]) continue;
-    if (d[k] > kLightDeg) nk[k] = (d[k] + kChunk - 1) / kChunk;
-    else ++nl;
-    nh += nk[k];
-  }
-  const uint32_t il = rb::warp_incl_scan(nl);
-  const uint32_t ih = rb::warp_incl_scan(nh);
-  const uint32_t tl = __shfl_sync(RB_FULL, il, 31);
-  const uint32_t th = __shfl_sync(RB_FULL, ih, 31);
-  if ((tl | th) == 0) return;
-  const uint32_t lane = rb::lane_id();
-  unsigned long long b = 0;
-  if (lane == 31 && tl) b = atomicAdd(lq_count, (unsigned long long)tl);
-  if (lane == 30 && th) b = atomicAdd(hq_count, (unsigned long long)th);
-  const unsigned long long bl = __shfl_sync(RB_FULL, b, 31);
-  const unsigned long long bh = __shfl_sync(RB_FULL, b, 30);
-  unsigned long long pl = bl + il - nl;
-#pragma unroll
-  for (int k = 0; k < KU; ++k) {
-    if (on[k] && d[k] <= kLightDeg) {
-      QEnt e;
-      e.s = s[k];
-      e.v = w[k];
-      e.d = (int32_t)d[k];
-      lq[pl++] = e;
-    }
-  }
-  for (uint32_t r = 0; r < th; r += 32) {
-    const uint32_t idx = r + lane;
-    const bool act = idx < th;
-    const uint32_t j = rb::warp_upper_bound(ih, act ? idx : th - 1);
-    uint32_t local = (act ? idx : th - 1) - (__shfl_sync(RB_FULL, ih, j) - __shfl_sync(RB_FULL, nh, j));
-    int32_t ew = 0;
-    int64_t es = 0;
-    uint32_t ed = 0;
-    bool got = false;
-#pragma unroll
-    for (int k = 0; k < KU; ++k) {
-      const uint32_t c = __shfl_sync(RB_FULL, nk[k], j);
-      const int32_t wk = __shfl_sync(RB_FULL, w[k], j);
-      const int64_t sk = rb::shfl_i64(s[k], j);
-      const uint32_t dk = __shfl_sync(RB_FULL, d[k], j);
-      if (!got && local < c) {
-        got = true;
-        ew = wk;
-        es = sk + (int64_t)local * kChunk;
-        ed = min(kChunk, dk - local * kChunk);
-      } else if (!got) {
-        local -= c;
-      }
-    }
-    if (act) {
-      QEnt e;
-      e.s = es;
-      e.v = ew;
-      e.d = (int32_t)ed;
-      hq[bh + idx] = e;
-    }
-  }
+// Top-down row record: one 32-byte sector per vertex (row start, degree and
+// the first two neighbours), so a scattered frontier costs one sector per row.
+__device__ __forceinline__ void ld_vinfo(const VInfo* q, int64_t& s, uint32_t& d, int32_t& n0, int32_t& n1) {
+  const int4 a = __ldg(reinterpret_cast<const int4*>(q));
+  const int4 b = __ldg(reinterpret_cast<const int4*>(q) + 1);
+  s = (int64_t)(((uint64_t)(uint32_t)a.y << 32) | (uint32_t)a.x);
+  d = (uint32_t)a.z;
+  n0 = a.w;
+  n1 = b.x;
 }
 
+__device__ __forceinline__ uint32_t nth_set_bit(uint32_t x, uint32_t k) {  // 0-based, LSB first
+  uint32_t pos = 0, c;
+  c = __popc(x & 0xffffu); if (k >= c) { k -= c; x >>= 16; pos += 16; }
+  c = __popc(x & 0xffu);   if (k >= c) { k -= c; x >>= 8;  pos += 8; }
+  c = __popc(x & 0xfu);    if (k >= c) { k -= c; x >>= 4;  pos += 4; }
+  c = __popc(x & 0x3u);    if (k >= c) { k -= c; x >>= 2;  pos += 2; }
+  c = x & 1u;              if (k >= c) { pos += 1; }
+  return pos;
+}
 
 // Warp-collective claim of KU edges per lane (v[k] -> w[k], act[k]).
 template <int KU>
 __device__ __forceinline__ void td_claim(const TdCtx& c, const int32_t (&v)[KU], const int32_t (&w)[KU],
                                          const bool (&act)[KU], Acc& acc) {
   const KParams& p = *c.p;
-  // claim = first to set the visited bit (vis holds every discovered vertex)
+  // claim = first to set the visited bit (vis holds every discovered vertex).
+  // A plain (L1-cacheable) probe filters already-visited targets first: bits
+  // only ever get set, so a stale probe can only cost an extra atomic.
+  uint32_t seen[KU];
+#pragma unroll
+  for (int k = 0; k < KU; ++k) seen[k] = act[k] ? ld_bits(p.vis + (w[k] >> 5)) : 0xffffffffu;
   bool claim[KU];
 #pragma unroll
   for (int k = 0; k < KU; ++k) {
     claim[k] = false;
-    if (act[k]) {
-      const uint32_t bit = 1u << (w[k] & 31);
+    const uint32_t bit = 1u << (w[k] & 31);
+    if (act[k] && !(seen[k] & bit)) {
       const uint32_t old = atomicOr(p.vis + (w[k] >> 5), bit);
       claim[k] = !(old & bit);
     }
@@ -283,95 +241,193 @@ __device__ __forceinline__ void td_claim(const TdCtx& c, const int32_t (&v)[KU],
   }
 }
 
-__device__ void td_level(const TdCtx& c, const QEnt* lq_in, const QEnt* hq_in, uint64_t nl,
-                         uint64_t nh, Acc& acc) {
+// Warp-aggregated append of hub rows (deg > kLightDeg) as kChunk-edge slices:
+// one atomic per warp reserves the range, all 32 lanes write slices in
+// parallel (a lane holding a huge row does not serialize the warp).
+template <int KU>
+__device__ __forceinline__ void warp_push_slices(QEnt* hq, unsigned long long* count, const int32_t (&w)[KU],
+                                                 const int64_t (&s)[KU], const uint32_t (&d)[KU],
+                                                 const bool (&hub)[KU]) {
+  uint32_t nh = 0;
+  uint32_t nk[KU];
+#pragma unroll
+  for (int k = 0; k < KU; ++k) {
+    nk[k] = hub[k] ? (d[k] + kChunk - 1) / kChunk : 0u;
+    nh += nk[k];
+  }
+  const uint32_t ih = rb::warp_incl_scan(nh);
+  const uint32_t th = __shfl_sync(RB_FULL, ih, 31);
+  if (th == 0) return;
+  const uint32_t lane = rb::lane_id();
+  unsigned long long b = 0;
+  if (lane == 31) b = atomicAdd(count, (unsigned long long)th);
+  const unsigned long long bh = __shfl_sync(RB_FULL, b, 31);
+  for (uint32_t r = 0; r < th; r += 32) {
+    const uint32_t idx = r + lane;
+    const bool act = idx < th;
+    const uint32_t j = rb::warp_upper_bound(ih, act ? idx : th - 1);
+    uint32_t local = (act ? idx : th - 1) - (__shfl_sync(RB_FULL, ih, j) - __shfl_sync(RB_FULL, nh, j));
+    int32_t ew = 0;
+    int64_t es = 0;
+    uint32_t ed = 0;
+    bool got = false;
+#pragma unroll
+    for (int k = 0; k < KU; ++k) {
+      const uint32_t cnt = __shfl_sync(RB_FULL, nk[k], j);
+      const int32_t wk = __shfl_sync(RB_FULL, w[k], j);
+      const int64_t sk = rb::shfl_i64(s[k], j);
+      const uint32_t dk = __shfl_sync(RB_FULL, d[k], j);
+      if (!got && local < cnt) {
+        got = true;
+        ew = wk;
+        es = sk + (int64_t)local * kChunk;
+        ed = min(kChunk, dk - local * kChunk);
+      } else if (!got) {
+        local -= cnt;
+      }
+    }
+    if (act) {
+      QEnt e;
+      e.s = es;
+      e.v = ew;
+      e.d = (int32_t)ed;
+      hq[bh + idx] = e;
+    }
+  }
+}
+
+// Top-down phase A: the frontier rows straight from the bitmap.  Two-level
+// walk: the lanes of a warp check 32 words of the nonzero summary (each covers
+// 32 bitmap words) strided over the whole range; inside a
+// nonzero summary word the set bits are enumerated across the lanes (prefix
+// sum + n-th set bit), 4 rows per lane per round.  Rows with deg <= 2 claim
+// their inline neighbours directly, rows with deg <= 32 are edge-balanced
+// across the warp (4 edges per lane per step), hub rows are appended as
+// 256-edge slices for phase B.
+__device__ void td_rows(const TdCtx& c, const uint32_t* nzcur, QEnt* hq, unsigned long long* hq_count, Acc& acc) {
   const KParams& p = *c.p;
   const uint32_t lane = rb::lane_id();
   const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
   const uint64_t gw = warp_slot();
-  const uint64_t nb = (nl + 31) / 32;
-  const uint64_t total = nb + nh;
-  // hub slices first (uniform size), then light batches
-  for (uint64_t item = gw; item < total; item += nwarps) {
-    if (item < nh) {
-      const QEnt ent = ld_qent(hq_in + item);
-      const int32_t v = ent.v;
-      const int64_t a = ent.s;
-      const int64_t b = a + ent.d;
-      if (lane == 0) acc.scan += (unsigned long long)(b - a);
-      int32_t vv[kChunkPerLane], w[kChunkPerLane];
-      bool act[kChunkPerLane];
-#pragma unroll
-      for (int k = 0; k < kChunkPerLane; ++k) {
-        const int64_t j = a + lane + 32 * k;
-        act[k] = j < b;
-        vv[k] = v;
-        w[k] = act[k] ? rb::ldg_i32(p.col + j) : 0;
-      }
-      td_claim<kChunkPerLane>(c, vv, w, act, acc);
-    } else {
-      const uint64_t idx = (item - nh) * 32 + lane;
-      int32_t v = 0;
-      int64_t s = 0;
-      uint32_t d = 0;
-      if (idx < nl) {
-        const QEnt ent = ld_qent(lq_in + idx);
-        v = ent.v;
-        s = ent.s;
-        d = (uint32_t)ent.d;
-      }
-      const uint32_t incl = rb::warp_incl_scan(d);
+  const uint64_t n_nz = (uint64_t)p.n_words / 32;
+  // lane l of warp g checks summary word g + (l + 32 i) * nwarps: one load
+  // skips 32 empty summary words, and the dense regions of a clustered (RCM)
+  // frontier are dealt round-robin over all warps
+  for (uint64_t j0 = gw; j0 < n_nz; j0 += nwarps * 32) {
+    const uint64_t jme = j0 + (uint64_t)lane * nwarps;
+    const uint32_t nzw = jme < n_nz ? __ldcg(nzcur + jme) : 0u;
+    for (uint32_t mask = __ballot_sync(RB_FULL, nzw != 0u); mask; mask &= mask - 1) {
+      const uint32_t jl = __ffs(mask) - 1;
+      const uint64_t wbase = (j0 + (uint64_t)jl * nwarps) * 32;  // first bitmap word of this summary word
+      const uint32_t bits = __shfl_sync(RB_FULL, nzw, jl);
+      const uint32_t x = ((bits >> lane) & 1u) ? __ldcg(c.fcur + wbase + lane) : 0u;
+      const uint32_t cnt = __popc(x);
+      const uint32_t incl = rb::warp_incl_scan(cnt);
       const uint32_t tot = __shfl_sync(RB_FULL, incl, 31);
-      const uint32_t excl = incl - d;
-      acc.scan += d;
-      for (uint32_t base = 0; base < tot; base += 32 * kTdUnroll) {
-        int32_t vv[kTdUnroll], w[kTdUnroll];
-        bool act[kTdUnroll];
+      const uint32_t excl = incl - cnt;
+      for (uint32_t r = 0; r < tot; r += 32 * kUB) {
+        int32_t v[kUB];
+        int64_t s0[kUB];
+        uint32_t d[kUB];
+        int32_t n0[kUB], n1[kUB];
+        bool on[kUB], hub[kUB];
 #pragma unroll
-        for (int k = 0; k < kTdUnroll; ++k) {
-          const uint32_t e = base + lane + 32 * k;
-          act[k] = e < tot;
-          const uint32_t j = rb::warp_upper_bound(incl, act[k] ? e : tot - 1);
-          vv[k] = __shfl_sync(RB_FULL, v, j);
-          const int64_t sj = rb::shfl_i64(s, j);
-          const uint32_t exj = __shfl_sync(RB_FULL, excl, j);
-          w[k] = act[k] ? rb::ldg_i32(p.col + sj + (e - exj)) : 0;
+        for (int k = 0; k < kUB; ++k) {
+          const uint32_t t = r + 32 * k + lane;
+          on[k] = t < tot;
+          const uint32_t o = rb::warp_upper_bound(incl, on[k] ? t : tot - 1);
+          const uint32_t xo = __shfl_sync(RB_FULL, x, o);
+          const uint32_t eo = __shfl_sync(RB_FULL, excl, o);
+          v[k] = (int32_t)((wbase + o) * 32 + nth_set_bit(xo, (on[k] ? t : tot - 1) - eo));
+          s0[k] = 0;
+          d[k] = 0;
+          n0[k] = n1[k] = 0;
+          if (on[k]) ld_vinfo(p.vinfo + v[k], s0[k], d[k], n0[k], n1[k]);
         }
-        td_claim<kTdUnroll>(c, vv, w, act, acc);
+        // rows with deg <= 2: neighbours are in the record
+        {
+          int32_t tv[2 * kUB], tw[2 * kUB];
+          bool ta[2 * kUB];
+#pragma unroll
+          for (int k = 0; k < kUB; ++k) {
+            const bool tiny = on[k] && d[k] >= 1 && d[k] <= kTinyDeg;
+            tv[2 * k] = tv[2 * k + 1] = v[k];
+            tw[2 * k] = n0[k];
+            tw[2 * k + 1] = n1[k];
+            ta[2 * k] = tiny;
+            ta[2 * k + 1] = tiny && d[k] == 2;
+            hub[k] = on[k] && d[k] > kLightDeg;
+            if (on[k] && !hub[k]) acc.scan += d[k];
+          }
+          td_claim<2 * kUB>(c, tv, tw, ta, acc);
+        }
+        // rows with 2 < deg <= 32: edge-balanced over the warp
+        uint32_t ld[kUB], lsum = 0;
+#pragma unroll
+        for (int k = 0; k < kUB; ++k) {
+          ld[k] = (on[k] && d[k] > kTinyDeg && d[k] <= kLightDeg) ? d[k] : 0u;
+          lsum += ld[k];
+        }
+        const uint32_t li = rb::warp_incl_scan(lsum);
+        const uint32_t lt = __shfl_sync(RB_FULL, li, 31);
+        for (uint32_t base = 0; base < lt; base += 32 * kTdUnroll) {
+          int32_t vv[kTdUnroll], w[kTdUnroll];
+          bool act[kTdUnroll];
+#pragma unroll
+          for (int q = 0; q < kTdUnroll; ++q) {
+            const uint32_t e = base + 32 * q + lane;
+            act[q] = e < lt;
+            const uint32_t ec = act[q] ? e : lt - 1;
+            const uint32_t o = rb::warp_upper_bound(li, ec);
+            uint32_t local = ec - (__shfl_sync(RB_FULL, li, o) - __shfl_sync(RB_FULL, lsum, o));
+            int32_t rv = 0;
+            int64_t rs0 = 0;
+            bool got = false;
+#pragma unroll
+            for (int k = 0; k < kUB; ++k) {
+              const uint32_t dk = __shfl_sync(RB_FULL, ld[k], o);
+              const int32_t vk = __shfl_sync(RB_FULL, v[k], o);
+              const int64_t sk = rb::shfl_i64(s0[k], o);
+              if (!got && local < dk) {
+                got = true;
+                rv = vk;
+                rs0 = sk + local;
+              } else if (!got) {
+                local -= dk;
+              }
+            }
+            vv[q] = rv;
+            w[q] = act[q] ? rb::ldg_i32(p.col + rs0) : 0;
+          }
+          td_claim<kTdUnroll>(c, vv, w, act, acc);
+        }
+        warp_push_slices<kUB>(hq, hq_count, v, s0, d, hub);
       }
     }
   }
 }
 
-// Bitmap -> queues at a bottom-up -> top-down switch.  Same lane mapping as
-// the bottom-up step (lane l <-> bit l of kUB consecutive words): one degree
-// load per set bit, kUB independent loads per lane, warp-aggregated appends.
-__device__ void compact_level(const KParams& p, const uint32_t* fcur, const uint32_t* nzcur, Slot* in, QEnt* lq,
-                              QEnt* hq) {
+// Top-down phase B: hub slices, one warp item each (8 edges per lane).
+__device__ void td_hubs(const TdCtx& c, const QEnt* hq, uint64_t nh, Acc& acc) {
+  const KParams& p = *c.p;
   const uint32_t lane = rb::lane_id();
   const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
-  const uint64_t gw = warp_slot();
-  const uint64_t nw = (uint64_t)p.n_words;
-  for (uint64_t w0 = gw * kUB; w0 < nw; w0 += nwarps * kUB) {
-    const uint32_t nzb = (ld_bits(nzcur + (w0 >> 5)) >> (w0 & 31)) & ((1u << kUB) - 1u);
-    if (!nzb) continue;  // no frontier vertex in these kUB words
-    const uint32_t x = (lane < kUB && ((nzb >> lane) & 1u)) ? __ldcg(fcur + w0 + lane) : 0u;
-    int32_t v[kUB];
-    int64_t s0[kUB];
-    uint32_t d[kUB];
-    bool on[kUB];
+  for (uint64_t item = warp_slot(); item < nh; item += nwarps) {
+    const QEnt ent = ld_qent(hq + item);
+    const int32_t v = ent.v;
+    const int64_t a = ent.s;
+    const int64_t b = a + ent.d;
+    if (lane == 0) acc.scan += (unsigned long long)(b - a);
+    int32_t vv[kChunkPerLane], w[kChunkPerLane];
+    bool act[kChunkPerLane];
 #pragma unroll
-    for (int k = 0; k < kUB; ++k) {
-      on[k] = (__shfl_sync(RB_FULL, x, k) >> lane) & 1u;
-      v[k] = (int32_t)((w0 + k) * 32 + lane);
-      s0[k] = 0;
-      d[k] = 0;
-      if (on[k]) {
-        s0[k] = rb::ldg_i64(p.rs + v[k]);
-        d[k] = (uint32_t)(rb::ldg_i64(p.rs + v[k] + 1) - s0[k]);
-      }
+    for (int k = 0; k < kChunkPerLane; ++k) {
+      const int64_t j = a + lane + 32 * k;
+      act[k] = j < b;
+      vv[k] = v;
+      w[k] = act[k] ? rb::ldg_i32(p.col + j) : 0;
     }
-    warp_append<kUB>(lq, &in->lq_count, hq, &in->hq_count, v, s0, d, on);
+    td_claim<kChunkPerLane>(c, vv, w, act, acc);
   }
 }
 
@@ -614,7 +670,7 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
   }
   int64_t done = 0;
   uint32_t epoch = 0;
-  uint64_t t_prev = 0;
+  uint64_t t_prev = 0, t_queue = 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) t_prev = globaltimer();
 
   while (done < p.max_levels && nf > 0) {
@@ -633,20 +689,19 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
 
     Acc acc{0, 0, 0};
     if (dir == 0) {
-      QEnt* lq_in = (L & 1) ? p.lq1 : p.lq0;
-      QEnt* hq_in = (L & 1) ? p.hq1 : p.hq0;
-      if (need_compact) {
-        compact_level(p, fcur, nz_of(p, L), in, lq_in, hq_in);
-        rb::grid_barrier(p.bar, nblocks, epoch);
-      }
+      QEnt* hq = (L & 1) ? p.hq1 : p.hq0;
       TdCtx c;
       c.p = &p;
       c.L = L;
       c.fcur = fcur;
       c.fnext = fnext;
       c.nznext = nz_of(p, L + 1);
-      c.out = out;
-      td_level(c, lq_in, hq_in, rb::ld_relaxed_u64(&in->lq_count), rb::ld_relaxed_u64(&in->hq_count), acc);
+      // phase A: frontier rows from the bitmap; hub rows become slices in hq
+      td_rows(c, nz_of(p, L), hq, &in->hq_count, acc);
+      rb::grid_barrier(p.bar, nblocks, epoch);
+      if (blockIdx.x == 0 && threadIdx.x == 0) t_queue = globaltimer() - t_prev;
+      // phase B: hub slices spread over all warps
+      td_hubs(c, hq, rb::ld_relaxed_u64(&in->hq_count), acc);
     } else {
       const uint32_t wib = threadIdx.x >> 5;
       bu_level<kRev>(p, L, fcur, fnext, nz_of(p, L + 1), acc, s_bu_found[wib], s_bu_pair[wib]);
@@ -667,7 +722,10 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
       r.scanned_edges = (int64_t)rb::ld_relaxed_u64(&out->scanned);
       r.t_ns = (int64_t)(t_now - t_prev);
       r.n_next = n_next;
+      r.t_queue_ns = (int64_t)t_queue;
+      r.reserved = 0;
       p.rec[done] = r;
+      t_queue = 0;
       t_prev = t_now;
     }
     // engine.py:587-596
@@ -705,26 +763,19 @@ __global__ void bfs_seed(KParams p, int64_t src) {
   p.fb0[src >> 5] |= 1u << (src & 31);
   p.nz0[src >> 10] |= 1u << ((src >> 5) & 31);
   p.vis[src >> 5] |= 1u << (src & 31);
-  const int64_t s0 = p.rs[src];
-  const uint32_t d = (uint32_t)(p.rs[src + 1] - s0);
-  Slot* in = p.slots + 2;  // inputs of level 0 = outputs of "level -1"
-  if (d > kLightDeg) {
-    uint32_t c = 0;
-    for (; c * kChunk < d; ++c) {
-      QEnt e;
-      e.s = s0 + (long long)c * kChunk;
-      e.v = (int32_t)src;
-      e.d = (int32_t)min(kChunk, d - c * kChunk);
-      p.hq0[c] = e;
-    }
-    in->hq_count = c;
-  } else {
-    QEnt e;
-    e.s = s0;
-    e.v = (int32_t)src;
-    e.d = (int32_t)d;
-    p.lq0[0] = e;
-    in->lq_count = 1;
+}
+
+// vinfo[v] = {row start, degree, first two neighbours} (top-down row record)
+__global__ void make_vinfo(const int64_t* rs, const int32_t* col, int64_t n, VInfo* vi) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = rs[v], e = rs[v + 1];
+    VInfo r;
+    r.s = s;
+    r.d = (int32_t)(e - s);
+    r.n0 = e - s > 0 ? col[s] : -1;
+    r.n1 = e - s > 1 ? col[s + 1] : -1;
+    r.pad[0] = r.pad[1] = r.pad[2] = 0;
+    vi[v] = r;
   }
 }
 
@@ -790,6 +841,7 @@ struct rb_bfs {
   uint32_t* vis_template;   // isolated + padding premarked
   uint32_t* pad_mask;       // padding bits only
   int2* hot;
+  VInfo* vinfo;
   int64_t n_full;  // words of a nonzero-summary bitmap (n_words / 32)
   int blocks;
   int sms;
@@ -858,10 +910,10 @@ extern "C" int rb_bfs_create(const int64_t* d_row_starts, const int32_t* d_col, 
   RB_ALLOC(k.nz0, (size_t)h->n_full * 4);
   RB_ALLOC(k.nz1, (size_t)h->n_full * 4);
   RB_ALLOC(k.nz2, (size_t)h->n_full * 4);
-  RB_ALLOC(k.lq0, (size_t)n_dev * sizeof(QEnt));
-  RB_ALLOC(k.lq1, (size_t)n_dev * sizeof(QEnt));
+  RB_ALLOC(h->vinfo, (size_t)n_dev * sizeof(VInfo));
   RB_ALLOC(k.hq0, nhub * sizeof(QEnt));
   RB_ALLOC(k.hq1, nhub * sizeof(QEnt));
+
   RB_ALLOC(k.parent, (size_t)n_dev * 4);
   RB_ALLOC(h->hot, (size_t)n_dev * sizeof(int2));
   RB_ALLOC(k.level, (size_t)n_dev * 4);
@@ -882,6 +934,8 @@ extern "C" int rb_bfs_create(const int64_t* d_row_starts, const int32_t* d_col, 
   make_pad_mask<<<256, 256>>>(h->pad_mask, n_dev, h->n_words);
   make_hot<<<1024, 256>>>(d_row_starts, k.col_bu, n_dev, params->bu_reverse, h->hot);
   k.hot = h->hot;
+  make_vinfo<<<1024, 256>>>(d_row_starts, d_col, n_dev, h->vinfo);
+  k.vinfo = h->vinfo;
   if (cudaMemcpy(h->vis_template, h->pad_mask, wb, cudaMemcpyDeviceToDevice) != cudaSuccess) {
     rb_set_error("rb_bfs_create: template copy failed");
     rb_bfs_destroy(h);
@@ -917,8 +971,8 @@ extern "C" int rb_bfs_create(const int64_t* d_row_starts, const int32_t* d_col, 
 extern "C" int rb_bfs_destroy(rb_bfs* h) {
   if (!h) return RB_OK;
   KParams& k = h->kp;
-  void* ptrs[] = {k.vis, k.fb0, k.fb1, k.fb2, h->vis_template, h->pad_mask, k.lq0, k.lq1, k.hq0, k.hq1,
-                  k.parent, k.level, k.slots, k.bar, k.rec, k.fin, k.nz0, k.nz1, k.nz2, h->hot};
+  void* ptrs[] = {k.vis, k.fb0, k.fb1, k.fb2, h->vis_template, h->pad_mask, k.hq0, k.hq1, k.parent,
+                  k.level, k.slots, k.bar, k.rec, k.fin, k.nz0, k.nz1, k.nz2, h->hot, h->vinfo};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete h;

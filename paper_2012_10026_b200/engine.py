@@ -139,6 +139,7 @@ class LevelRecord:
     pass1_hits: int | None = None
     live_vertices: int | None = None
     claimed: int | None = None
+    queue_time: float = 0.0  # device seconds of this level spent rebuilding top-down queues
 
 
 @dataclass
@@ -290,7 +291,7 @@ def _records_to_levels(recs) -> list:
             LevelRecord(
                 level=int(r.level), direction=TOP_DOWN if r.direction == 0 else BOTTOM_UP, n_f=int(r.n_f),
                 m_f=int(r.m_f), m_u=int(r.m_u), scanned_edges=int(r.scanned_edges), wall_time=r.t_ns * 1e-9,
-                per_thread_edges=np.array([int(r.scanned_edges)], dtype=np.int64),
+                per_thread_edges=np.array([int(r.scanned_edges)], dtype=np.int64), queue_time=r.t_queue_ns * 1e-9,
             )
         )
     return out

@@ -35,4 +35,4 @@ with rb.BfsEngine(g2, rb.BfsParams(mode=a.mode)) as eng:
         el_s, levels = eng.run_device(int(s))
         print(f"root {s}: {el_s*1e6:.1f} us, levels {len(levels)}")
         for r in levels:
-            print(f"   L{r.level} {r.direction[:1].upper()} n_f={r.n_f:9d} m_f={r.m_f:11d} scanned={r.scanned_edges:11d} t={r.wall_time*1e6:8.1f}us")
+            print(f"   L{r.level} {r.direction[:1].upper()} n_f={r.n_f:9d} m_f={r.m_f:11d} scanned={r.scanned_edges:11d} t={r.wall_time*1e6:8.1f}us (queue {r.queue_time*1e6:6.1f})")
