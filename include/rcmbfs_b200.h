@@ -101,6 +101,8 @@ int rb_bfs_destroy(rb_bfs* h);
 int rb_bfs_reset(rb_bfs* h, int64_t source, void* stream);
 /* The traversal (engine.py:534-598): one cooperative persistent launch. */
 int rb_bfs_traverse(rb_bfs* h, void* stream);
+/* Device time of the last traversal (all of its launches), seconds. */
+int rb_bfs_elapsed(rb_bfs* h, double* seconds);
 /* Copy results; parents/levels cover [0,n_dev); n_records <= cap. */
 int rb_bfs_results(rb_bfs* h, int32_t* d_or_h_parent, int32_t* d_or_h_level, rb_level_record* h_records,
                    int64_t cap, int64_t* n_records, void* stream);
@@ -115,6 +117,10 @@ int32_t* rb_bfs_level_ptr(rb_bfs* h);
 int rb_bfs_grid(rb_bfs* h, int* blocks, int* threads);
 /* Diagnostics: average cost of one grid barrier of the traversal grid. */
 int rb_bfs_barrier_probe(rb_bfs* h, int iters, double* ns_per_barrier, void* stream);
+/* Diagnostics (engine created with RB_DEBUG_TS set): per level (first 64),
+ * per CTA: globaltimer at level start, after the work + block reduction,
+ * after the grid barrier, 0. */
+int rb_bfs_debug_timestamps(rb_bfs* h, uint64_t* out, int64_t cap, int* blocks);
 
 #ifdef __cplusplus
 }

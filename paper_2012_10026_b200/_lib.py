@@ -54,12 +54,14 @@ _SIGS = {
     "rb_bfs_destroy": ([P], ctypes.c_int),
     "rb_bfs_reset": ([P, I64, P], ctypes.c_int),
     "rb_bfs_traverse": ([P, P], ctypes.c_int),
+    "rb_bfs_elapsed": ([P, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
     "rb_bfs_results": ([P, P, P, P, I64, ctypes.POINTER(I64), P], ctypes.c_int),
     "rb_bfs_step": ([P, ctypes.c_int, P, P, P, P, P, P, P, P], ctypes.c_int),
     "rb_bfs_parent_ptr": ([P], P),
     "rb_bfs_level_ptr": ([P], P),
     "rb_bfs_grid": ([P, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "rb_bfs_barrier_probe": ([P, ctypes.c_int, ctypes.POINTER(ctypes.c_double), P], ctypes.c_int),
+    "rb_bfs_debug_timestamps": ([P, P, I64, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
 }
 
 EXPORTED = tuple(_SIGS)

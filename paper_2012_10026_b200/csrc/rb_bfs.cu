@@ -87,7 +87,8 @@ struct Slot {  // per-level counters, triple-buffered by level % 3
   unsigned long long deg_next;
   unsigned long long scanned;
   unsigned long long hq_count;  // hub slices appended by phase A of the NEXT level
-  unsigned long long pad0, pad1, pad2, pad3;
+  unsigned long long maxdeg;    // max degree of the next frontier (hub slices needed?)
+  unsigned long long pad1, pad2, pad3;
 };
 
 struct Final {  // state after a launch (continuation for very deep graphs)
@@ -124,6 +125,7 @@ struct KParams {
   rb_level_record* rec;
   Final* fin;
   int alpha, beta, hybrid, debug;
+  unsigned long long* dbg;
   int64_t n_policy;
   // start state
   int64_t level0;
@@ -157,6 +159,7 @@ __device__ __forceinline__ uint64_t globaltimer() {
 
 struct Acc {
   unsigned long long n, deg, scan;
+  uint32_t maxdeg;
 };
 
 // Global warp index, interleaved across blocks: consecutive work items go to
@@ -171,6 +174,7 @@ struct TdCtx {
   const uint32_t* fcur;
   uint32_t* fnext;
   uint32_t* nznext;
+  bool probe;  // probe visited bits before the atomic (most targets visited)
 };
 
 __device__ __forceinline__ QEnt ld_qent(const QEnt* q) {
@@ -209,11 +213,12 @@ __device__ __forceinline__ void td_claim(const TdCtx& c, const int32_t (&v)[KU],
                                          const bool (&act)[KU], Acc& acc) {
   const KParams& p = *c.p;
   // claim = first to set the visited bit (vis holds every discovered vertex).
-  // A plain (L1-cacheable) probe filters already-visited targets first: bits
-  // only ever get set, so a stale probe can only cost an extra atomic.
+  // Late levels (most targets already visited) first probe with a plain,
+  // L1-cacheable load -- bits only ever get set, so a stale probe can only
+  // cost an extra atomic; early levels go straight to the atomic.
   uint32_t seen[KU];
 #pragma unroll
-  for (int k = 0; k < KU; ++k) seen[k] = act[k] ? ld_bits(p.vis + (w[k] >> 5)) : 0xffffffffu;
+  for (int k = 0; k < KU; ++k) seen[k] = (act[k] && c.probe) ? ld_bits(p.vis + (w[k] >> 5)) : 0u;
   bool claim[KU];
 #pragma unroll
   for (int k = 0; k < KU; ++k) {
@@ -224,6 +229,10 @@ __device__ __forceinline__ void td_claim(const TdCtx& c, const int32_t (&v)[KU],
       claim[k] = !(old & bit);
     }
   }
+  // the degree loads of the winners are issued before the frontier atomics
+  uint32_t dw[KU];
+#pragma unroll
+  for (int k = 0; k < KU; ++k) dw[k] = claim[k] ? (uint32_t)rb::ldg_i32(p.deg + w[k]) : 0u;
 #pragma unroll
   for (int k = 0; k < KU; ++k) {
     if (!claim[k]) continue;
@@ -236,7 +245,8 @@ __device__ __forceinline__ void td_claim(const TdCtx& c, const int32_t (&v)[KU],
   for (int k = 0; k < KU; ++k) {
     if (claim[k]) {
       acc.n += 1;
-      acc.deg += (uint32_t)rb::ldg_i32(p.deg + w[k]);
+      acc.deg += dw[k];
+      acc.maxdeg = max(acc.maxdeg, dw[k]);
     }
   }
 }
@@ -309,18 +319,19 @@ __device__ void td_rows(const TdCtx& c, const uint32_t* nzcur, QEnt* hq, unsigne
   const uint32_t lane = rb::lane_id();
   const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
   const uint64_t gw = warp_slot();
-  const uint64_t n_nz = (uint64_t)p.n_words / 32;
-  // lane l of warp g checks summary word g + (l + 32 i) * nwarps: one load
-  // skips 32 empty summary words, and the dense regions of a clustered (RCM)
-  // frontier are dealt round-robin over all warps
-  for (uint64_t j0 = gw; j0 < n_nz; j0 += nwarps * 32) {
-    const uint64_t jme = j0 + (uint64_t)lane * nwarps;
-    const uint32_t nzw = jme < n_nz ? __ldcg(nzcur + jme) : 0u;
-    for (uint32_t mask = __ballot_sync(RB_FULL, nzw != 0u); mask; mask &= mask - 1) {
-      const uint32_t jl = __ffs(mask) - 1;
-      const uint64_t wbase = (j0 + (uint64_t)jl * nwarps) * 32;  // first bitmap word of this summary word
-      const uint32_t bits = __shfl_sync(RB_FULL, nzw, jl);
-      const uint32_t x = ((bits >> lane) & 1u) ? __ldcg(c.fcur + wbase + lane) : 0u;
+  // work item = 8 consecutive bitmap words (256 vertices) = one byte of the
+  // nonzero summary.  Lane l of warp g checks item g + (l + 32 i) * nwarps:
+  // one load skips 32 empty items, and the dense regions of a clustered (RCM)
+  // frontier are dealt round-robin over all warps.
+  const uint64_t n_items = (uint64_t)p.n_words / 8;
+  for (uint64_t i0 = gw; i0 < n_items; i0 += nwarps * 32) {
+    const uint64_t ime = i0 + (uint64_t)lane * nwarps;
+    const uint32_t nzb = ime < n_items ? (ld_bits(nzcur + (ime >> 2)) >> (8 * (ime & 3))) & 0xffu : 0u;
+    for (uint32_t mask = __ballot_sync(RB_FULL, nzb != 0u); mask; mask &= mask - 1) {
+      const uint32_t il = __ffs(mask) - 1;
+      const uint64_t wbase = (i0 + (uint64_t)il * nwarps) * 8;  // first bitmap word of this item
+      const uint32_t bits = __shfl_sync(RB_FULL, nzb, il);
+      const uint32_t x = (lane < 8 && ((bits >> lane) & 1u)) ? __ldcg(c.fcur + wbase + lane) : 0u;
       const uint32_t cnt = __popc(x);
       const uint32_t incl = rb::warp_incl_scan(cnt);
       const uint32_t tot = __shfl_sync(RB_FULL, incl, 31);
@@ -538,6 +549,7 @@ __device__ void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uint
         p.level[vbase + 32 * k] = (int32_t)(L + 1);
         acc.n += 1;
         acc.deg += dg[k];
+        acc.maxdeg = max(acc.maxdeg, dg[k]);
       }
     }
     // Longer rows that did not hit: the (lane, k) pairs are compacted across
@@ -609,6 +621,7 @@ __device__ void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uint
           p.level[v] = (int32_t)(L + 1);
           acc.n += 1;
           acc.deg += d;
+          acc.maxdeg = max(acc.maxdeg, d);
           atomicOr(fm_s + (idx >> 5), 1u << (idx & 31));
         }
       }
@@ -637,23 +650,31 @@ __device__ __forceinline__ void block_add3(unsigned long long* red, const Acc& a
   const unsigned long long A = rb::warp_sum_u64(a.n);
   const unsigned long long B = rb::warp_sum_u64(a.deg);
   const unsigned long long C = rb::warp_sum_u64(a.scan);
+  const uint32_t M = __reduce_max_sync(RB_FULL, a.maxdeg);
   const uint32_t w = threadIdx.x >> 5;
   if (rb::lane_id() == 0) {
-    red[w * 3 + 0] = A;
-    red[w * 3 + 1] = B;
-    red[w * 3 + 2] = C;
+    red[w * 4 + 0] = A;
+    red[w * 4 + 1] = B;
+    red[w * 4 + 2] = C;
+    red[w * 4 + 3] = M;
   }
   __syncthreads();
-  if (threadIdx.x < 3) {
+  if (threadIdx.x < 4) {
     unsigned long long s = 0;
-    for (int i = 0; i < kWarps; ++i) s += red[i * 3 + threadIdx.x];
-    if (s) atomicAdd(threadIdx.x == 0 ? &out->n_next : (threadIdx.x == 1 ? &out->deg_next : &out->scanned), s);
+    for (int i = 0; i < kWarps; ++i) {
+      const unsigned long long x = red[i * 4 + threadIdx.x];
+      s = threadIdx.x == 3 ? (x > s ? x : s) : s + x;
+    }
+    if (s) {
+      if (threadIdx.x == 3) atomicMax(&out->maxdeg, s);
+      else atomicAdd(threadIdx.x == 0 ? &out->n_next : (threadIdx.x == 1 ? &out->deg_next : &out->scanned), s);
+    }
   }
 }
 
 template <bool kRev>
 __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
-  __shared__ unsigned long long s_red[kWarps * 3];
+  __shared__ unsigned long long s_red[kWarps * 4];
   __shared__ uint32_t s_bu_found[kWarps][kBU];
   __shared__ uint32_t s_bu_pair[kWarps][32 * kBU];
   const uint32_t nblocks = gridDim.x;
@@ -670,6 +691,9 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
   }
   int64_t done = 0;
   uint32_t epoch = 0;
+  // does the current frontier hold a row longer than kLightDeg?  Level 0: the
+  // source's degree; a continuation launch conservatively assumes yes.
+  bool hubs = (p.mf0 < 0) ? (mf > (int64_t)kLightDeg) : true;
   uint64_t t_prev = 0, t_queue = 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) t_prev = globaltimer();
 
@@ -681,13 +705,14 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
     uint32_t* fzero = fb_of(p, L + 2);
     uint32_t* nzzero = nz_of(p, L + 2);
     // zero ahead: next level's fnext bitmap (+ summary) and the counter slot of level L+1
+    const uint64_t tA = globaltimer();
     for (uint64_t i = gtid; i < (uint64_t)p.n_words / 4; i += gthreads)
       reinterpret_cast<uint4*>(fzero)[i] = make_uint4(0u, 0u, 0u, 0u);
     for (uint64_t i = gtid; i < (uint64_t)p.n_words / 32; i += gthreads) nzzero[i] = 0u;
     if (blockIdx.x == 0 && threadIdx.x < sizeof(Slot) / 8)
       reinterpret_cast<unsigned long long*>(p.slots + ((L + 1) % 3))[threadIdx.x] = 0ull;
 
-    Acc acc{0, 0, 0};
+    Acc acc{0, 0, 0, 0u};
     if (dir == 0) {
       QEnt* hq = (L & 1) ? p.hq1 : p.hq0;
       TdCtx c;
@@ -696,21 +721,33 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
       c.fcur = fcur;
       c.fnext = fnext;
       c.nznext = nz_of(p, L + 1);
+      c.probe = 2 * mu < p.m_directed;  // fewer than half the edge ends unvisited
       // phase A: frontier rows from the bitmap; hub rows become slices in hq
       td_rows(c, nz_of(p, L), hq, &in->hq_count, acc);
-      rb::grid_barrier(p.bar, nblocks, epoch);
-      if (blockIdx.x == 0 && threadIdx.x == 0) t_queue = globaltimer() - t_prev;
-      // phase B: hub slices spread over all warps
-      td_hubs(c, hq, rb::ld_relaxed_u64(&in->hq_count), acc);
+      if (hubs) {  // phase B only if some frontier row has more than kLightDeg edges
+        rb::grid_barrier(p.bar, nblocks, epoch);
+        if (blockIdx.x == 0 && threadIdx.x == 0) t_queue = globaltimer() - t_prev;
+        td_hubs(c, hq, rb::ld_relaxed_u64(&in->hq_count), acc);
+      }
     } else {
       const uint32_t wib = threadIdx.x >> 5;
       bu_level<kRev>(p, L, fcur, fnext, nz_of(p, L + 1), acc, s_bu_found[wib], s_bu_pair[wib]);
     }
     block_add3(s_red, acc, out);
+    const uint64_t tB = globaltimer();
     rb::grid_barrier(p.bar, nblocks, epoch);
+    if (p.dbg && threadIdx.x == 0 && done < 64) {  // RB_DEBUG_TS: per-block phase timestamps
+      const uint64_t tC = globaltimer();
+      unsigned long long* d = p.dbg + ((uint64_t)done * gridDim.x + blockIdx.x) * 4;
+      d[0] = tA;
+      d[1] = tB;
+      d[2] = tC;
+      d[3] = 0;
+    }
 
     const int64_t n_next = (int64_t)rb::ld_relaxed_u64(&out->n_next);
     const int64_t deg_next = (int64_t)rb::ld_relaxed_u64(&out->deg_next);
+    hubs = rb::ld_relaxed_u64(&out->maxdeg) > kLightDeg;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       const uint64_t t_now = globaltimer();
       rb_level_record r;
@@ -849,6 +886,7 @@ struct rb_bfs {
   int64_t source;
   std::vector<rb_level_record> recs;
   int64_t levels_per_launch;  // kRecCap; RB_LEVELS_PER_LAUNCH=1 gives one launch per level (profiling)
+  cudaEvent_t ev_start, ev_end;  // bracket all launches of one traversal
   bool launched;
   void* stream;
 };
@@ -882,7 +920,10 @@ extern "C" int rb_bfs_create(const int64_t* d_row_starts, const int32_t* d_col, 
   h->bu_reverse = params->bu_reverse;
   h->launched = false;
   h->levels_per_launch = kRecCap;
+  cudaEventCreate(&h->ev_start);
+  cudaEventCreate(&h->ev_end);
   if (const char* env = getenv("RB_DEBUG")) h->kp.debug = atoi(env);
+  h->kp.dbg = nullptr;
   if (const char* env = getenv("RB_LEVELS_PER_LAUNCH")) {
     const long long v = atoll(env);
     if (v >= 1 && v <= kRecCap) h->levels_per_launch = v;
@@ -921,6 +962,7 @@ extern "C" int rb_bfs_create(const int64_t* d_row_starts, const int32_t* d_col, 
   RB_ALLOC(k.bar, 64);
   RB_ALLOC(k.rec, kRecCap * sizeof(rb_level_record));
   RB_ALLOC(k.fin, sizeof(Final));
+  if (getenv("RB_DEBUG_TS")) RB_ALLOC(k.dbg, (size_t)64 * 4 * 8 * 1024);
 #undef RB_ALLOC
   if (rc != RB_OK) {
     rb_bfs_destroy(h);
@@ -972,9 +1014,11 @@ extern "C" int rb_bfs_destroy(rb_bfs* h) {
   if (!h) return RB_OK;
   KParams& k = h->kp;
   void* ptrs[] = {k.vis, k.fb0, k.fb1, k.fb2, h->vis_template, h->pad_mask, k.hq0, k.hq1, k.parent,
-                  k.level, k.slots, k.bar, k.rec, k.fin, k.nz0, k.nz1, k.nz2, h->hot, h->vinfo};
+                  k.level, k.slots, k.bar, k.rec, k.fin, k.nz0, k.nz1, k.nz2, h->hot, h->vinfo, k.dbg};
   for (void* q : ptrs)
     if (q) cudaFree(q);
+  if (h->ev_start) cudaEventDestroy(h->ev_start);
+  if (h->ev_end) cudaEventDestroy(h->ev_end);
   delete h;
   return RB_OK;
 }
@@ -1048,7 +1092,11 @@ extern "C" int rb_bfs_traverse(rb_bfs* h, void* stream) {
   if (!h) return RB_ERR_ARG;
   h->launched = true;
   h->stream = stream;
-  return launch(h, (cudaStream_t)stream, 0, 0, 0, h->levels_per_launch, 1, -1, 0);
+  RB_CUDA_TRY(cudaEventRecord(h->ev_start, (cudaStream_t)stream));
+  int rc = launch(h, (cudaStream_t)stream, 0, 0, 0, h->levels_per_launch, 1, -1, 0);
+  if (rc) return rc;
+  RB_CUDA_TRY(cudaEventRecord(h->ev_end, (cudaStream_t)stream));
+  return RB_OK;
 }
 
 extern "C" int rb_bfs_results(rb_bfs* h, int32_t* parent_out, int32_t* level_out, rb_level_record* h_records,
@@ -1072,6 +1120,7 @@ extern "C" int rb_bfs_results(rb_bfs* h, int32_t* parent_out, int32_t* level_out
       RB_CUDA_TRY(cudaMemsetAsync(h->kp.bar, 0, 64, s));
       int rc = launch(h, s, f.L, f.dir, f.need_compact, h->levels_per_launch, f.nf, f.mf, f.mu);
       if (rc) return rc;
+      RB_CUDA_TRY(cudaEventRecord(h->ev_end, s));
     }
     h->launched = false;
   }
@@ -1143,5 +1192,22 @@ extern "C" int rb_bfs_barrier_probe(rb_bfs* h, int iters, double* ns_per_barrier
   cudaEventDestroy(b);
   RB_CUDA_TRY(cudaMemsetAsync(h->kp.bar, 0, 64, s));
   *ns_per_barrier = 1e6 * (double)ms / iters;
+  return RB_OK;
+}
+
+extern "C" int rb_bfs_debug_timestamps(rb_bfs* h, uint64_t* out, int64_t cap, int* blocks) {
+  if (!h || !h->kp.dbg) return RB_ERR_ARG;
+  const int64_t n = (int64_t)64 * 4 * h->blocks;
+  RB_CUDA_TRY(cudaMemcpy(out, h->kp.dbg, (size_t)(n < cap ? n : cap) * 8, cudaMemcpyDeviceToHost));
+  *blocks = h->blocks;
+  return RB_OK;
+}
+
+extern "C" int rb_bfs_elapsed(rb_bfs* h, double* seconds) {
+  if (!h || !seconds) return RB_ERR_ARG;
+  float ms = 0.f;
+  RB_CUDA_TRY(cudaEventSynchronize(h->ev_end));
+  RB_CUDA_TRY(cudaEventElapsedTime(&ms, h->ev_start, h->ev_end));
+  *seconds = 1e-3 * (double)ms;
   return RB_OK;
 }

@@ -232,8 +232,6 @@ class _DeviceBfs:
         )
         self.pinned = torch.empty(n_dev, dtype=torch.int32, pin_memory=True)
         self._recs = (_lib.LevelRecordC * 256)()
-        self.ev0 = torch.cuda.Event(enable_timing=True)
-        self.ev1 = torch.cuda.Event(enable_timing=True)
 
     def close(self):
         if self.h:
@@ -251,9 +249,7 @@ class _DeviceBfs:
         L = _lib.lib()
         s = _lib.stream_ptr()
         _lib.check(L.rb_bfs_reset(self.h, int(source), s), "rb_bfs_reset")
-        self.ev0.record()
         _lib.check(L.rb_bfs_traverse(self.h, s), "rb_bfs_traverse")
-        self.ev1.record()
 
     def results(self, want_parent=True, level_out=None, parent_host=None):
         """Drain the traversal; copy parents (to ``parent_host`` numpy int32
@@ -275,8 +271,9 @@ class _DeviceBfs:
             self._recs = (_lib.LevelRecordC * nrec.value)()
             _lib.check(L.rb_bfs_results(self.h, None, None, self._recs, len(self._recs), ctypes.byref(nrec),
                                         _lib.stream_ptr()), "rb_bfs_results")
-        elapsed = self.ev0.elapsed_time(self.ev1) / 1000.0
-        return self._recs[: nrec.value], elapsed
+        el = ctypes.c_double(0.0)
+        _lib.check(L.rb_bfs_elapsed(self.h, ctypes.byref(el)), "rb_bfs_elapsed")  # all launches of the traversal
+        return self._recs[: nrec.value], el.value
 
     def level_tensor(self):
         """Device int32 level array over [0, n_dev) (valid after results())."""

@@ -15,6 +15,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--scale", type=int, default=22)
 ap.add_argument("--roots", type=int, default=4)
 ap.add_argument("--mode", default="hybrid")
+ap.add_argument("--flush", action="store_true", help="write 256 MiB before each root (cold L2, like bench.py)")
 a = ap.parse_args()
 el = rb.kronecker_generate(rb.KroneckerParams(scale=a.scale))
 g = rb.build_csr(el)
@@ -31,7 +32,11 @@ with rb.BfsEngine(g2, rb.BfsParams(mode=a.mode)) as eng:
         _lib.check(_lib.lib().rb_bfs_barrier_probe(eng._dev.h, it, ctypes.byref(ns), _lib.stream_ptr()))
         print(f"grid {blocks.value}x{threads.value}: barrier {ns.value:.0f} ns (iters={it})")
     eng.run_device(int(roots[0]))
+    import torch
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for s in roots[: a.roots]:
+        if a.flush:
+            flush.zero_()
         el_s, levels = eng.run_device(int(s))
         print(f"root {s}: {el_s*1e6:.1f} us, levels {len(levels)}")
         for r in levels:
