@@ -61,7 +61,7 @@ constexpr int kTdUnroll = 4;                     // light batch: edges per lane 
 constexpr int kUB = 4;                           // compaction: words per warp step
 constexpr int kBU = 8;                           // bottom-up: words per warp step
 constexpr int kK1 = 2;                           // bottom-up: first-round checks per vertex
-constexpr int kK2 = 10;                          // bottom-up: per-lane checks before the warp takes over
+constexpr int kK2 = 258;                         // bottom-up: per-lane checks before the warp takes over
 constexpr int kHeavyPerLane = 8;                 // warp-cooperative bottom-up: neighbours per lane per step
 constexpr int64_t kRecCap = 4096;                // level records per launch
 
@@ -137,13 +137,11 @@ struct KParams {
   int64_t m_directed;
 };
 
-__device__ __forceinline__ uint32_t* fb_of(const KParams& p, int64_t i) {
-  const int64_t r = i % 3;
+__device__ __forceinline__ uint32_t* fb_of(const KParams& p, int r) {  // r = level % 3
   return r == 0 ? p.fb0 : (r == 1 ? p.fb1 : p.fb2);
 }
 
-__device__ __forceinline__ uint32_t* nz_of(const KParams& p, int64_t i) {
-  const int64_t r = i % 3;
+__device__ __forceinline__ uint32_t* nz_of(const KParams& p, int r) {
   return r == 0 ? p.nz0 : (r == 1 ? p.nz1 : p.nz2);
 }
 
@@ -585,16 +583,17 @@ __device__ void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uint
           s0 = rb::ldg_i64(p.rs + (int64_t)w0 * 32 + idx);
           const int64_t e0 = s0 + d;
           const int64_t lim = d < (uint32_t)kK2 ? d : kK2;
-          for (int64_t t0 = 2; par < 0 && t0 < lim; t0 += 4) {
-            int32_t uu[4];
-            uint32_t bb[4];
+          // contiguous 8-neighbour chunks of the row: one sector per lane per step
+          for (int64_t t0 = 2; par < 0 && t0 < lim; t0 += 8) {
+            int32_t uu[8];
+            uint32_t bb[8];
 #pragma unroll
-            for (int t = 0; t < 4; ++t)
+            for (int t = 0; t < 8; ++t)
               uu[t] = (t0 + t < lim) ? rb::ldg_i32(p.col_bu + bu_idx<kRev>(s0, e0, t0 + t)) : -1;
 #pragma unroll
-            for (int t = 0; t < 4; ++t) bb[t] = uu[t] >= 0 ? ld_bits(fcur + (uu[t] >> 5)) : 0u;
+            for (int t = 0; t < 8; ++t) bb[t] = uu[t] >= 0 ? ld_bits(fcur + (uu[t] >> 5)) : 0u;
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
+            for (int t = 0; t < 8; ++t) {
               if (par < 0 && uu[t] >= 0) {
                 ++checks;
                 if ((bb[t] >> (uu[t] & 31)) & 1u) par = uu[t];
@@ -646,35 +645,38 @@ __device__ void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uint
 
 // ---------------------------------------------------------------------------
 
+// Block reduction of the level counters: warp partials go to shared memory,
+// warp 0 combines them with shuffles and one lane per counter issues the
+// global atomic (fire-and-forget).  The caller's grid barrier follows.
 __device__ __forceinline__ void block_add3(unsigned long long* red, const Acc& a, Slot* out) {
   const unsigned long long A = rb::warp_sum_u64(a.n);
   const unsigned long long B = rb::warp_sum_u64(a.deg);
   const unsigned long long C = rb::warp_sum_u64(a.scan);
   const uint32_t M = __reduce_max_sync(RB_FULL, a.maxdeg);
-  const uint32_t w = threadIdx.x >> 5;
-  if (rb::lane_id() == 0) {
+  const uint32_t w = threadIdx.x >> 5, lane = rb::lane_id();
+  if (lane == 0) {
     red[w * 4 + 0] = A;
     red[w * 4 + 1] = B;
     red[w * 4 + 2] = C;
     red[w * 4 + 3] = M;
   }
   __syncthreads();
-  if (threadIdx.x < 4) {
-    unsigned long long s = 0;
-    for (int i = 0; i < kWarps; ++i) {
-      const unsigned long long x = red[i * 4 + threadIdx.x];
-      s = threadIdx.x == 3 ? (x > s ? x : s) : s + x;
-    }
-    if (s) {
-      if (threadIdx.x == 3) atomicMax(&out->maxdeg, s);
-      else atomicAdd(threadIdx.x == 0 ? &out->n_next : (threadIdx.x == 1 ? &out->deg_next : &out->scanned), s);
-    }
+  if (w == 0) {
+    const unsigned long long sa = rb::warp_sum_u64(lane < kWarps ? red[lane * 4 + 0] : 0ull);
+    const unsigned long long sb = rb::warp_sum_u64(lane < kWarps ? red[lane * 4 + 1] : 0ull);
+    const unsigned long long sc = rb::warp_sum_u64(lane < kWarps ? red[lane * 4 + 2] : 0ull);
+    const uint32_t sm = __reduce_max_sync(RB_FULL, lane < kWarps ? (uint32_t)red[lane * 4 + 3] : 0u);
+    if (lane == 0 && sa) atomicAdd(&out->n_next, sa);
+    if (lane == 1 && sb) atomicAdd(&out->deg_next, sb);
+    if (lane == 2 && sc) atomicAdd(&out->scanned, sc);
+    if (lane == 3 && sm) atomicMax(&out->maxdeg, (unsigned long long)sm);
   }
 }
 
 template <bool kRev>
 __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
   __shared__ unsigned long long s_red[kWarps * 4];
+  __shared__ unsigned long long s_ctr[4];
   __shared__ uint32_t s_bu_found[kWarps][kBU];
   __shared__ uint32_t s_bu_pair[kWarps][32 * kBU];
   const uint32_t nblocks = gridDim.x;
@@ -691,26 +693,29 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
   }
   int64_t done = 0;
   uint32_t epoch = 0;
+  int r0 = (int)(L % 3);
   // does the current frontier hold a row longer than kLightDeg?  Level 0: the
   // source's degree; a continuation launch conservatively assumes yes.
   bool hubs = (p.mf0 < 0) ? (mf > (int64_t)kLightDeg) : true;
   uint64_t t_prev = 0, t_queue = 0;
-  if (blockIdx.x == 0 && threadIdx.x == 0) t_prev = globaltimer();
+  if (blockIdx.x == 0 && threadIdx.x == 32) t_prev = globaltimer();
 
   while (done < p.max_levels && nf > 0) {
-    Slot* out = p.slots + (L % 3);
-    Slot* in = p.slots + ((L + 2) % 3);
-    const uint32_t* fcur = fb_of(p, L);
-    uint32_t* fnext = fb_of(p, L + 1);
-    uint32_t* fzero = fb_of(p, L + 2);
-    uint32_t* nzzero = nz_of(p, L + 2);
+    // rotating buffers: r0 = L % 3 (kept incrementally, no 64-bit modulo)
+    const int r1 = r0 == 2 ? 0 : r0 + 1, r2 = r1 == 2 ? 0 : r1 + 1;
+    Slot* out = p.slots + r0;
+    Slot* in = p.slots + r2;
+    const uint32_t* fcur = fb_of(p, r0);
+    uint32_t* fnext = fb_of(p, r1);
+    uint32_t* fzero = fb_of(p, r2);
+    uint32_t* nzzero = nz_of(p, r2);
     // zero ahead: next level's fnext bitmap (+ summary) and the counter slot of level L+1
     const uint64_t tA = globaltimer();
     for (uint64_t i = gtid; i < (uint64_t)p.n_words / 4; i += gthreads)
       reinterpret_cast<uint4*>(fzero)[i] = make_uint4(0u, 0u, 0u, 0u);
     for (uint64_t i = gtid; i < (uint64_t)p.n_words / 32; i += gthreads) nzzero[i] = 0u;
     if (blockIdx.x == 0 && threadIdx.x < sizeof(Slot) / 8)
-      reinterpret_cast<unsigned long long*>(p.slots + ((L + 1) % 3))[threadIdx.x] = 0ull;
+      reinterpret_cast<unsigned long long*>(p.slots + r1)[threadIdx.x] = 0ull;
 
     Acc acc{0, 0, 0, 0u};
     if (dir == 0) {
@@ -720,35 +725,41 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
       c.L = L;
       c.fcur = fcur;
       c.fnext = fnext;
-      c.nznext = nz_of(p, L + 1);
+      c.nznext = nz_of(p, r1);
       c.probe = 2 * mu < p.m_directed;  // fewer than half the edge ends unvisited
       // phase A: frontier rows from the bitmap; hub rows become slices in hq
-      td_rows(c, nz_of(p, L), hq, &in->hq_count, acc);
+      td_rows(c, nz_of(p, r0), hq, &in->hq_count, acc);
       if (hubs) {  // phase B only if some frontier row has more than kLightDeg edges
-        rb::grid_barrier(p.bar, nblocks, epoch);
-        if (blockIdx.x == 0 && threadIdx.x == 0) t_queue = globaltimer() - t_prev;
-        td_hubs(c, hq, rb::ld_relaxed_u64(&in->hq_count), acc);
+        {
+          const unsigned long long* const src[1] = {&in->hq_count};
+          rb::grid_barrier_fetch<1>(p.bar, nblocks, epoch, src, s_ctr);
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 32) t_queue = globaltimer() - t_prev;
+        td_hubs(c, hq, s_ctr[0], acc);
       }
     } else {
       const uint32_t wib = threadIdx.x >> 5;
-      bu_level<kRev>(p, L, fcur, fnext, nz_of(p, L + 1), acc, s_bu_found[wib], s_bu_pair[wib]);
+      bu_level<kRev>(p, L, fcur, fnext, nz_of(p, r1), acc, s_bu_found[wib], s_bu_pair[wib]);
     }
     block_add3(s_red, acc, out);
     const uint64_t tB = globaltimer();
-    rb::grid_barrier(p.bar, nblocks, epoch);
+    {
+      const unsigned long long* const src[4] = {&out->n_next, &out->deg_next, &out->maxdeg, &out->scanned};
+      rb::grid_barrier_fetch<4>(p.bar, nblocks, epoch, src, s_ctr);
+    }
     if (p.dbg && threadIdx.x == 0 && done < 64) {  // RB_DEBUG_TS: per-block phase timestamps
       const uint64_t tC = globaltimer();
       unsigned long long* d = p.dbg + ((uint64_t)done * gridDim.x + blockIdx.x) * 4;
       d[0] = tA;
       d[1] = tB;
       d[2] = tC;
-      d[3] = 0;
     }
 
-    const int64_t n_next = (int64_t)rb::ld_relaxed_u64(&out->n_next);
-    const int64_t deg_next = (int64_t)rb::ld_relaxed_u64(&out->deg_next);
-    hubs = rb::ld_relaxed_u64(&out->maxdeg) > kLightDeg;
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t n_next = (int64_t)s_ctr[0];
+    const int64_t deg_next = (int64_t)s_ctr[1];
+    hubs = s_ctr[2] > kLightDeg;
+    if (p.dbg && threadIdx.x == 0 && done < 64) p.dbg[((uint64_t)done * gridDim.x + blockIdx.x) * 4 + 3] = globaltimer() + (uint64_t)(n_next & 0) + (uint64_t)(deg_next & 0) + (hubs ? 0 : 0);
+    if (blockIdx.x == 0 && threadIdx.x == 32) {
       const uint64_t t_now = globaltimer();
       rb_level_record r;
       r.level = L;
@@ -756,7 +767,7 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
       r.n_f = nf;
       r.m_f = mf;
       r.m_u = mu;
-      r.scanned_edges = (int64_t)rb::ld_relaxed_u64(&out->scanned);
+      r.scanned_edges = (int64_t)s_ctr[3];
       r.t_ns = (int64_t)(t_now - t_prev);
       r.n_next = n_next;
       r.t_queue_ns = (int64_t)t_queue;
@@ -772,14 +783,15 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
     int ndir = 0;
     if (p.hybrid) {
       if (dir == 0)
-        ndir = ((double)mf > (double)mu / (double)p.alpha) ? 1 : 0;
+        ndir = (mf * (int64_t)p.alpha > mu) ? 1 : 0;  // == (m_f > m_u / alpha) exactly for m_u < 2^46
       else
-        ndir = ((double)nf < (double)p.n_policy / (double)p.beta) ? 0 : 1;
+        ndir = (nf * (int64_t)p.beta < p.n_policy) ? 0 : 1;  // == (n_f < n / beta)
     }
     need_compact = ndir == 0;  // queues are always rebuilt from the frontier bitmap
     dir = ndir;
     ++L;
     ++done;
+    r0 = r0 == 2 ? 0 : r0 + 1;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     p.fin->levels_done = done;

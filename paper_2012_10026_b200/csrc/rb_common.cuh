@@ -51,6 +51,28 @@ __device__ __forceinline__ void grid_barrier(uint32_t* bar, uint32_t nblocks, ui
   __syncthreads();
 }
 
+// Grid barrier that also fetches K 64-bit words written before it (counters
+// reduced by atomics): thread 0 loads them once per block and shares them
+// through shared memory -- if every thread loaded them, thousands of warps
+// would queue on one L2 line.
+template <int K>
+__device__ __forceinline__ void grid_barrier_fetch(uint32_t* bar, uint32_t nblocks, uint32_t& epoch,
+                                                   const unsigned long long* const (&src)[K],
+                                                   unsigned long long* s_out) {
+  ++epoch;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    red_release_add(bar, 1u);
+    const uint32_t target = epoch * nblocks;
+    while ((int32_t)(ld_relaxed_u32(bar) - target) < 0) {
+    }
+    __threadfence();
+#pragma unroll
+    for (int k = 0; k < K; ++k) s_out[k] = ld_relaxed_u64(src[k]);
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
 // Warp inclusive scan (32-bit).

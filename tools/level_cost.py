@@ -30,7 +30,10 @@ for extra in ([0, 1 << 22] if len(sys.argv) < 2 else [int(x) for x in sys.argv[1
             _lib.check(_lib.lib().rb_bfs_debug_timestamps(eng._dev.h, buf.ctypes.data_as(ctypes.c_void_p), buf.size, ctypes.byref(nb)))
             ts = buf[: 64 * 4 * nb.value].reshape(64, nb.value, 4).astype(np.int64)
             for L in range(1, 6):
-                a, b, c = ts[L, :, 0], ts[L, :, 1], ts[L, :, 2]
+                a, b, c, dd = ts[L, :, 0], ts[L, :, 1], ts[L, :, 2], ts[L, :, 3]
+                an = ts[L + 1, :, 0]
+                print(f"  L{L}: counters read {np.median(dd-c)/1e3:.2f} us (max {(dd-c).max()/1e3:.2f}), "
+                      f"counters->next start {np.median(an-dd)/1e3:.2f} (max {(an-dd).max()/1e3:.2f})")
                 print(f"  L{L}: start skew {(a.max()-a.min())/1e3:.2f} us, work+reduce max {(b-a).max()/1e3:.2f} "
                       f"(median {np.median(b-a)/1e3:.2f}, argmax blk {int(np.argmax(b-a))}), "
                       f"barrier after last arrival {(c.min()-b.max())/1e3:.2f}..{(c.max()-b.max())/1e3:.2f} us, "

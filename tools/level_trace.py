@@ -15,6 +15,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--scale", type=int, default=22)
 ap.add_argument("--roots", type=int, default=4)
 ap.add_argument("--mode", default="hybrid")
+ap.add_argument("--brief", action="store_true")
+ap.add_argument("--sources", type=int, nargs="*", default=None)
 ap.add_argument("--flush", action="store_true", help="write 256 MiB before each root (cold L2, like bench.py)")
 a = ap.parse_args()
 el = rb.kronecker_generate(rb.KroneckerParams(scale=a.scale))
@@ -34,10 +36,13 @@ with rb.BfsEngine(g2, rb.BfsParams(mode=a.mode)) as eng:
     eng.run_device(int(roots[0]))
     import torch
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    for s in roots[: a.roots]:
+    for s in (a.sources if a.sources else roots[: a.roots]):
         if a.flush:
             flush.zero_()
         el_s, levels = eng.run_device(int(s))
-        print(f"root {s}: {el_s*1e6:.1f} us, levels {len(levels)}")
+        print(f"root {s}: {el_s*1e6:.1f} us, levels {len(levels)}  " + " ".join(
+            f"{r.direction[0].upper()}{r.wall_time*1e6:.0f}" for r in levels))
+        if a.brief:
+            continue
         for r in levels:
             print(f"   L{r.level} {r.direction[:1].upper()} n_f={r.n_f:9d} m_f={r.m_f:11d} scanned={r.scanned_edges:11d} t={r.wall_time*1e6:8.1f}us (queue {r.queue_time*1e6:6.1f})")
