@@ -238,12 +238,18 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    one_gpu = os.environ.get("RB_BENCH_ONE_GPU") == "1"  # debug: all ranks share cuda:0, gloo collectives
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     # ---- preprocessing (timed separately, reported, not part of the metric)
     t0 = time.perf_counter()
@@ -279,6 +285,9 @@ def run_ours(args):
     raw = np.array(raw, np.int64)
     del lab, el
 
+    if world > 1:
+        return run_partitioned(args, rb, torch, dist, g2, stats, roots, raw, world, rank,
+                               {"generate": t_gen, "csr_build": t_csr, "rcm_plus_relabel": t_rcm})
     eng = rb.BfsEngine(g2, rb.BfsParams(mode=args.mode))
     n_dev = eng.n_dev
     n_plus_dev = stats.n_non_isolated
@@ -387,6 +396,90 @@ def run_ours(args):
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def run_partitioned(args, rb, torch, dist, g2, stats, roots, raw, world, rank, prep):
+    """--gpus N > 1: ONE traversal per root over the 1D vertex-block partition
+    (distributed.py): per level a local step per GPU + NCCL counter all-reduce
+    and frontier-bitmap all-gather.  Per-root time = max over ranks (device
+    events), value = harmonic mean over roots (strong scaling: same graph,
+    same roots)."""
+    from paper_2012_10026_b200.distributed import GpuLocalLevel, PartitionedBfs, partition_bounds
+
+    n_plus = stats.n_non_isolated
+    rs_host = g2.row_starts
+    deg_host = g2.degrees
+    bounds = partition_bounds(rs_host, n_plus, world)
+    local = GpuLocalLevel(g2, bounds, rank, alpha=64, beta=8, hybrid=args.mode != "level_sync")
+    drv = PartitionedBfs(local, bounds, rank, world, n_policy=g2.n, m_directed=g2.m_directed,
+                         hybrid=args.mode != "level_sync")
+    k = args.steps if args.profile_roots == 0 else args.profile_roots
+    order = list(range(64))
+    my = [order[i % 64] for i in range(k)]
+    for i in range(args.warmup):
+        drv.run(int(roots[my[i % len(my)]]), int(deg_host[roots[my[i % len(my)]]]))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    ev_a = torch.cuda.Event(enable_timing=True)
+    ev_b = torch.cuda.Event(enable_timing=True)
+    times, teps, alg, nlev = [], [], [], []
+    dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        for j in my:
+            flush.zero_()
+            dist.barrier()
+            torch.cuda.synchronize()
+            ev_a.record()
+            recs = drv.run(int(roots[j]), int(deg_host[roots[j]]))
+            ev_b.record()
+            torch.cuda.synchronize()
+            t = torch.tensor([ev_a.elapsed_time(ev_b) / 1e3], dtype=torch.float64, device=drv.local.device)
+            if drv.stage:
+                t = t.cpu()
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+            times.append(el)
+            teps.append(raw[j] / el)
+            levels = [type("R", (), dict(direction="top_down" if r.direction == 0 else "bottom_up", n_f=r.n_f,
+                                         scanned_edges=r.scanned))() for r in recs]
+            alg.append(algorithmic_bytes(levels, n_plus, n_plus))
+            nlev.append(len(recs))
+    # e2e: the same traversal + each rank's parent slice copied to host
+    e2e = []
+    for j in my[: min(len(my), 8)]:
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        drv.run(int(roots[j]), int(deg_host[roots[j]]))
+        _ = local.parents().cpu().numpy()
+        t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64)
+        if not drv.stage:
+            t = t.cuda()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e.append(raw[j] / float(t.item()))
+    if rank == 0:
+        peak, peak_kind = measured_peak()
+        ach = float(np.sum(alg) / np.sum(times) / 1e9) / world  # per GPU
+        line = {
+            "metric": METRIC, "value": hmean(teps) / 1e9, "unit": UNIT, "n_gpus": world, "steps": len(my),
+            "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic Kronecker (reference generator, seed 1), built on device",
+            "config": {"workload": f"kronecker-s{args.scale}-ef{args.edgefactor}-rcm-bfs", "scale": args.scale,
+                       "edgefactor": args.edgefactor, "roots": len(my), "mode": args.mode,
+                       "parallelism": f"1d-partition x{world} (NCCL all-gather / all-reduce per level)",
+                       "partition_bounds": bounds, "l2": "flushed (256 MiB write) before every root"},
+            "preprocessing_s": prep,
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                         "peak_kind": peak_kind, "kernel": "bfs_persistent (per GPU)", "traffic": None},
+            "e2e": {"value": hmean(e2e) / 1e9, "unit": UNIT, "h2d_bytes_per_step": 8,
+                    "d2h_bytes_per_step": int(4 * (bounds[1] - bounds[0]))},
+            "gpu_launches": int(sum(2 * x + 1 for x in nlev)),  # per root: seed + per level (step + summary)
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    local.close()
+    dist.destroy_process_group()
 
 
 def main():

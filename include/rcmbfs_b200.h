@@ -97,6 +97,37 @@ int rb_bfs_create(const int64_t* d_row_starts, const int32_t* d_col, const int32
                   const int32_t* d_degrees, int64_t n_dev, const uint32_t* d_isolated_words,
                   const rb_bfs_params* params, rb_bfs** out);
 int rb_bfs_destroy(rb_bfs* h);
+
+/* 1D vertex-block partition (multi-GPU): this engine owns global
+ * vertices [v_lo, v_lo + n_dev); its CSR rows (d_row_starts local, columns
+ * GLOBAL ids) serve bottom-up; top-down expands every global frontier vertex
+ * through the transpose slice d_td_row_starts / d_td_col (the owned
+ * neighbours of each of the n_glob global vertices). */
+typedef struct {
+  int64_t v_lo;
+  int64_t n_glob;
+  const int64_t* d_td_row_starts;
+  const int32_t* d_td_col;
+} rb_bfs_partition;
+int rb_bfs_create_part(const int64_t* d_row_starts, const int32_t* d_col, const int32_t* d_col_bu,
+                       const int32_t* d_degrees, int64_t n_dev, const uint32_t* d_isolated_words,
+                       const rb_bfs_params* params, const rb_bfs_partition* part, rb_bfs** out);
+/* Partitioned traversal, driven level by level by the host (which exchanges
+ * frontier bitmaps and counters, e.g. with NCCL): reset (seeds the source if
+ * owned), then one level from the all-gathered global frontier bitmap (+ its
+ * nonzero summary, rb_make_nz).  Returns the local next-frontier words and the
+ * local counters n_next, deg_next, maxdeg, scanned. */
+int rb_bfs_reset_part(rb_bfs* h, int64_t source_global, void* stream);
+int rb_bfs_dist_level(rb_bfs* h, int64_t level, int direction, int hubs, const uint32_t* d_fcur_glob,
+                      const uint32_t* d_nz_glob, uint32_t** d_next_local, int64_t* h_counters, void* stream);
+int rb_bfs_words(rb_bfs* h, int64_t* n_words_local, int64_t* n_words_glob);
+int rb_make_nz(const uint32_t* d_words, int64_t n_words, uint32_t* d_nz, void* stream);
+/* Transpose slice for a partition: for every global vertex u < n_glob, the
+ * owned vertices adjacent to u (ascending). */
+size_t rb_transpose_workspace_bytes(int64_t m_local, int64_t n_glob);
+int rb_transpose_rows(const int64_t* d_row_starts_local, const int32_t* d_col_local, int64_t n_local, int64_t v_lo,
+                      int64_t m_local, int64_t n_glob, void* d_ws, size_t ws_bytes, int64_t* d_td_row_starts,
+                      int32_t* d_td_col, void* stream);
 /* Reset per-root state (not timed; engine.py:526-532). */
 int rb_bfs_reset(rb_bfs* h, int64_t source, void* stream);
 /* The traversal (engine.py:534-598): one cooperative persistent launch. */

@@ -37,6 +37,10 @@ class BfsParamsC(ctypes.Structure):
     ]
 
 
+class PartitionC(ctypes.Structure):
+    _fields_ = [("v_lo", I64), ("n_glob", I64), ("d_td_row_starts", P), ("d_td_col", P)]
+
+
 _SIGS = {
     "rb_last_error": ([], ctypes.c_char_p),
     "rb_version": ([], ctypes.c_int),
@@ -52,6 +56,14 @@ _SIGS = {
     "rb_degree_sort_adjacency": ([P, P, P, I64, I64, ctypes.c_int, P, SZ, P, P], ctypes.c_int),
     "rb_bfs_create": ([P, P, P, P, I64, P, ctypes.POINTER(BfsParamsC), ctypes.POINTER(P)], ctypes.c_int),
     "rb_bfs_destroy": ([P], ctypes.c_int),
+    "rb_bfs_create_part": ([P, P, P, P, I64, P, ctypes.POINTER(BfsParamsC), ctypes.POINTER(PartitionC),
+                            ctypes.POINTER(P)], ctypes.c_int),
+    "rb_bfs_reset_part": ([P, I64, P], ctypes.c_int),
+    "rb_bfs_dist_level": ([P, I64, ctypes.c_int, ctypes.c_int, P, P, ctypes.POINTER(P), P, P], ctypes.c_int),
+    "rb_bfs_words": ([P, ctypes.POINTER(I64), ctypes.POINTER(I64)], ctypes.c_int),
+    "rb_make_nz": ([P, I64, P, P], ctypes.c_int),
+    "rb_transpose_workspace_bytes": ([I64, I64], SZ),
+    "rb_transpose_rows": ([P, P, I64, I64, I64, I64, P, SZ, P, P, P], ctypes.c_int),
     "rb_bfs_reset": ([P, I64, P], ctypes.c_int),
     "rb_bfs_traverse": ([P, P], ctypes.c_int),
     "rb_bfs_elapsed": ([P, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),

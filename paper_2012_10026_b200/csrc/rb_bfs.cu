@@ -115,7 +115,18 @@ struct KParams {
   uint32_t* nz0;   // bit i: fb0 word i is nonzero -- lets the queue build skip empty words
   uint32_t* nz1;
   uint32_t* nz2;
-  const VInfo* vinfo;  // top-down row records
+  const VInfo* vinfo;  // top-down row records (single GPU: of the graph itself)
+  // 1D partition (multi-GPU): this engine owns global vertices [v_lo, v_lo + n_dev);
+  // top-down expands every GLOBAL frontier vertex through the transpose slice
+  // (td_vinfo / td_col: the owned neighbours of each global vertex).  Single
+  // GPU: v_lo = 0, td_* = the graph, n_words_glob = n_words.
+  int64_t v_lo;
+  int64_t n_words_glob;
+  const VInfo* td_vinfo;
+  const int32_t* td_col;
+  const uint32_t* fcur_ext;   // if set: the (all-gathered) global frontier bitmap of this level
+  const uint32_t* nzcur_ext;  // and its nonzero summary
+  int64_t hubs0;              // -1: derive from deg(src); 0 / 1: forced (distributed levels)
   QEnt* hq0;           // hub slices of the current top-down level (alternating)
   QEnt* hq1;
   int32_t* parent;
@@ -210,34 +221,38 @@ template <int KU>
 __device__ __forceinline__ void td_claim(const TdCtx& c, const int32_t (&v)[KU], const int32_t (&w)[KU],
                                          const bool (&act)[KU], Acc& acc) {
   const KParams& p = *c.p;
+  // targets are global ids of OWNED vertices; local index = w - v_lo
+  int32_t wl[KU];
+#pragma unroll
+  for (int k = 0; k < KU; ++k) wl[k] = w[k] - (int32_t)p.v_lo;
   // claim = first to set the visited bit (vis holds every discovered vertex).
   // Late levels (most targets already visited) first probe with a plain,
   // L1-cacheable load -- bits only ever get set, so a stale probe can only
   // cost an extra atomic; early levels go straight to the atomic.
   uint32_t seen[KU];
 #pragma unroll
-  for (int k = 0; k < KU; ++k) seen[k] = (act[k] && c.probe) ? ld_bits(p.vis + (w[k] >> 5)) : 0u;
+  for (int k = 0; k < KU; ++k) seen[k] = (act[k] && c.probe) ? ld_bits(p.vis + (wl[k] >> 5)) : 0u;
   bool claim[KU];
 #pragma unroll
   for (int k = 0; k < KU; ++k) {
     claim[k] = false;
-    const uint32_t bit = 1u << (w[k] & 31);
+    const uint32_t bit = 1u << (wl[k] & 31);
     if (act[k] && !(seen[k] & bit)) {
-      const uint32_t old = atomicOr(p.vis + (w[k] >> 5), bit);
+      const uint32_t old = atomicOr(p.vis + (wl[k] >> 5), bit);
       claim[k] = !(old & bit);
     }
   }
   // the degree loads of the winners are issued before the frontier atomics
   uint32_t dw[KU];
 #pragma unroll
-  for (int k = 0; k < KU; ++k) dw[k] = claim[k] ? (uint32_t)rb::ldg_i32(p.deg + w[k]) : 0u;
+  for (int k = 0; k < KU; ++k) dw[k] = claim[k] ? (uint32_t)rb::ldg_i32(p.deg + wl[k]) : 0u;
 #pragma unroll
   for (int k = 0; k < KU; ++k) {
     if (!claim[k]) continue;
-    p.parent[w[k]] = v[k];
-    p.level[w[k]] = (int32_t)(c.L + 1);
-    const uint32_t old = atomicOr(c.fnext + (w[k] >> 5), 1u << (w[k] & 31));
-    if (old == 0u) atomicOr(c.nznext + (w[k] >> 10), 1u << ((w[k] >> 5) & 31));
+    p.parent[wl[k]] = v[k];
+    p.level[wl[k]] = (int32_t)(c.L + 1);
+    const uint32_t old = atomicOr(c.fnext + (wl[k] >> 5), 1u << (wl[k] & 31));
+    if (old == 0u) atomicOr(c.nznext + (wl[k] >> 10), 1u << ((wl[k] >> 5) & 31));
   }
 #pragma unroll
   for (int k = 0; k < KU; ++k) {
@@ -321,7 +336,7 @@ __device__ void td_rows(const TdCtx& c, const uint32_t* nzcur, QEnt* hq, unsigne
   // nonzero summary.  Lane l of warp g checks item g + (l + 32 i) * nwarps:
   // one load skips 32 empty items, and the dense regions of a clustered (RCM)
   // frontier are dealt round-robin over all warps.
-  const uint64_t n_items = (uint64_t)p.n_words / 8;
+  const uint64_t n_items = (uint64_t)p.n_words_glob / 8;
   for (uint64_t i0 = gw; i0 < n_items; i0 += nwarps * 32) {
     const uint64_t ime = i0 + (uint64_t)lane * nwarps;
     const uint32_t nzb = ime < n_items ? (ld_bits(nzcur + (ime >> 2)) >> (8 * (ime & 3))) & 0xffu : 0u;
@@ -351,7 +366,7 @@ __device__ void td_rows(const TdCtx& c, const uint32_t* nzcur, QEnt* hq, unsigne
           s0[k] = 0;
           d[k] = 0;
           n0[k] = n1[k] = 0;
-          if (on[k]) ld_vinfo(p.vinfo + v[k], s0[k], d[k], n0[k], n1[k]);
+          if (on[k]) ld_vinfo(p.td_vinfo + v[k], s0[k], d[k], n0[k], n1[k]);
         }
         // rows with deg <= 2: neighbours are in the record
         {
@@ -406,7 +421,7 @@ __device__ void td_rows(const TdCtx& c, const uint32_t* nzcur, QEnt* hq, unsigne
               }
             }
             vv[q] = rv;
-            w[q] = act[q] ? rb::ldg_i32(p.col + rs0) : 0;
+            w[q] = act[q] ? rb::ldg_i32(p.td_col + rs0) : 0;
           }
           td_claim<kTdUnroll>(c, vv, w, act, acc);
         }
@@ -434,7 +449,7 @@ __device__ void td_hubs(const TdCtx& c, const QEnt* hq, uint64_t nh, Acc& acc) {
       const int64_t j = a + lane + 32 * k;
       act[k] = j < b;
       vv[k] = v;
-      w[k] = act[k] ? rb::ldg_i32(p.col + j) : 0;
+      w[k] = act[k] ? rb::ldg_i32(p.td_col + j) : 0;
     }
     td_claim<kChunkPerLane>(c, vv, w, act, acc);
   }
@@ -696,7 +711,7 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
   int r0 = (int)(L % 3);
   // does the current frontier hold a row longer than kLightDeg?  Level 0: the
   // source's degree; a continuation launch conservatively assumes yes.
-  bool hubs = (p.mf0 < 0) ? (mf > (int64_t)kLightDeg) : true;
+  bool hubs = p.hubs0 >= 0 ? p.hubs0 != 0 : ((p.mf0 < 0) ? (mf > (int64_t)kLightDeg) : true);
   uint64_t t_prev = 0, t_queue = 0;
   if (blockIdx.x == 0 && threadIdx.x == 32) t_prev = globaltimer();
 
@@ -705,7 +720,7 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
     const int r1 = r0 == 2 ? 0 : r0 + 1, r2 = r1 == 2 ? 0 : r1 + 1;
     Slot* out = p.slots + r0;
     Slot* in = p.slots + r2;
-    const uint32_t* fcur = fb_of(p, r0);
+    const uint32_t* fcur = p.fcur_ext ? p.fcur_ext : fb_of(p, r0);
     uint32_t* fnext = fb_of(p, r1);
     uint32_t* fzero = fb_of(p, r2);
     uint32_t* nzzero = nz_of(p, r2);
@@ -728,7 +743,7 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
       c.nznext = nz_of(p, r1);
       c.probe = 2 * mu < p.m_directed;  // fewer than half the edge ends unvisited
       // phase A: frontier rows from the bitmap; hub rows become slices in hq
-      td_rows(c, nz_of(p, r0), hq, &in->hq_count, acc);
+      td_rows(c, p.nzcur_ext ? p.nzcur_ext : nz_of(p, r0), hq, &in->hq_count, acc);
       if (hubs) {  // phase B only if some frontier row has more than kLightDeg edges
         {
           const unsigned long long* const src[1] = {&in->hq_count};
@@ -891,6 +906,8 @@ struct rb_bfs {
   uint32_t* pad_mask;       // padding bits only
   int2* hot;
   VInfo* vinfo;
+  VInfo* td_vinfo;  // partitioned engines only
+  int64_t n_glob;
   int64_t n_full;  // words of a nonzero-summary bitmap (n_words / 32)
   int blocks;
   int sms;
@@ -912,9 +929,9 @@ static int alloc_dev(void** p, size_t bytes) {
   return RB_OK;
 }
 
-extern "C" int rb_bfs_create(const int64_t* d_row_starts, const int32_t* d_col, const int32_t* d_col_bu,
-                             const int32_t* d_degrees, int64_t n_dev, const uint32_t* d_isolated_words,
-                             const rb_bfs_params* params, rb_bfs** out) {
+extern "C" int rb_bfs_create_part(const int64_t* d_row_starts, const int32_t* d_col, const int32_t* d_col_bu,
+                                  const int32_t* d_degrees, int64_t n_dev, const uint32_t* d_isolated_words,
+                                  const rb_bfs_params* params, const rb_bfs_partition* part, rb_bfs** out) {
   if (!out || !params || n_dev <= 0 || !d_row_starts || !d_col || !d_degrees) {
     rb_set_error("rb_bfs_create: invalid argument");
     return RB_ERR_ARG;
@@ -990,6 +1007,26 @@ extern "C" int rb_bfs_create(const int64_t* d_row_starts, const int32_t* d_col, 
   k.hot = h->hot;
   make_vinfo<<<1024, 256>>>(d_row_starts, d_col, n_dev, h->vinfo);
   k.vinfo = h->vinfo;
+  k.hubs0 = -1;
+  if (part) {
+    const int64_t tile_g = 32 * 32 * kBU;
+    k.v_lo = part->v_lo;
+    k.n_words_glob = ((part->n_glob + tile_g - 1) / tile_g) * (tile_g / 32);
+    if (alloc_dev((void**)&h->td_vinfo, (size_t)part->n_glob * sizeof(VInfo)) != RB_OK) {
+      rb_bfs_destroy(h);
+      return RB_ERR_OOM;
+    }
+    make_vinfo<<<1024, 256>>>(part->d_td_row_starts, part->d_td_col, part->n_glob, h->td_vinfo);
+    k.td_vinfo = h->td_vinfo;
+    k.td_col = part->d_td_col;
+    h->n_glob = part->n_glob;
+  } else {
+    k.v_lo = 0;
+    k.n_words_glob = h->n_words;
+    k.td_vinfo = h->vinfo;
+    k.td_col = d_col;
+    h->n_glob = n_dev;
+  }
   if (cudaMemcpy(h->vis_template, h->pad_mask, wb, cudaMemcpyDeviceToDevice) != cudaSuccess) {
     rb_set_error("rb_bfs_create: template copy failed");
     rb_bfs_destroy(h);
@@ -1026,7 +1063,7 @@ extern "C" int rb_bfs_destroy(rb_bfs* h) {
   if (!h) return RB_OK;
   KParams& k = h->kp;
   void* ptrs[] = {k.vis, k.fb0, k.fb1, k.fb2, h->vis_template, h->pad_mask, k.hq0, k.hq1, k.parent,
-                  k.level, k.slots, k.bar, k.rec, k.fin, k.nz0, k.nz1, k.nz2, h->hot, h->vinfo, k.dbg};
+                  k.level, k.slots, k.bar, k.rec, k.fin, k.nz0, k.nz1, k.nz2, h->hot, h->vinfo, k.dbg, h->td_vinfo};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (h->ev_start) cudaEventDestroy(h->ev_start);
@@ -1221,5 +1258,95 @@ extern "C" int rb_bfs_elapsed(rb_bfs* h, double* seconds) {
   RB_CUDA_TRY(cudaEventSynchronize(h->ev_end));
   RB_CUDA_TRY(cudaEventElapsedTime(&ms, h->ev_start, h->ev_end));
   *seconds = 1e-3 * (double)ms;
+  return RB_OK;
+}
+
+extern "C" int rb_bfs_create(const int64_t* d_row_starts, const int32_t* d_col, const int32_t* d_col_bu,
+                             const int32_t* d_degrees, int64_t n_dev, const uint32_t* d_isolated_words,
+                             const rb_bfs_params* params, rb_bfs** out) {
+  return rb_bfs_create_part(d_row_starts, d_col, d_col_bu, d_degrees, n_dev, d_isolated_words, params, nullptr, out);
+}
+
+// ---- 1D-partition levels: the host drives the level loop and the exchange ----
+
+extern "C" int rb_bfs_reset_part(rb_bfs* h, int64_t source_global, void* stream) {
+  if (!h) return RB_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = reset_common(h, s);
+  if (rc) return rc;
+  RB_CUDA_TRY(cudaMemcpyAsync(h->kp.vis, h->vis_template, (size_t)h->n_words * 4, cudaMemcpyDeviceToDevice, s));
+  const int64_t local = source_global - h->kp.v_lo;
+  if (local >= 0 && local < h->n_dev) {
+    bfs_seed<<<1, 32, 0, s>>>(h->kp, local);
+    RB_CUDA_TRY(cudaGetLastError());
+  }
+  h->source = local;
+  h->recs.clear();
+  h->launched = false;
+  return RB_OK;
+}
+
+extern "C" int rb_bfs_dist_level(rb_bfs* h, int64_t level, int direction, int hubs, const uint32_t* d_fcur_glob,
+                                 const uint32_t* d_nz_glob, uint32_t** d_next_local, int64_t* h_counters,
+                                 void* stream) {
+  if (!h || !d_fcur_glob || !d_nz_glob || (direction != 0 && direction != 1)) {
+    rb_set_error("rb_bfs_dist_level: invalid argument");
+    return RB_ERR_ARG;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  RB_CUDA_TRY(cudaMemsetAsync(h->kp.bar, 0, 64, s));
+  KParams kp = h->kp;
+  kp.level0 = level;
+  kp.dir0 = direction;
+  kp.need_compact0 = 0;
+  kp.max_levels = 1;
+  kp.nf0 = 1;
+  kp.mf0 = 0;
+  kp.mu0 = 0;
+  kp.src = 0;
+  kp.m_directed = h->prm.m_directed;
+  kp.fcur_ext = d_fcur_glob;
+  kp.nzcur_ext = d_nz_glob;
+  kp.hubs0 = hubs ? 1 : 0;
+  void* args[] = {&kp};
+  cudaError_t e;
+  if (h->bu_reverse)
+    e = cudaLaunchCooperativeKernel((const void*)bfs_persistent<true>, dim3(h->blocks), dim3(kThreads), args, 0, s);
+  else
+    e = cudaLaunchCooperativeKernel((const void*)bfs_persistent<false>, dim3(h->blocks), dim3(kThreads), args, 0, s);
+  if (e != cudaSuccess) {
+    rb_set_error("cooperative launch failed: %s", cudaGetErrorString(e));
+    return RB_ERR_CUDA;
+  }
+  Slot sl;
+  RB_CUDA_TRY(cudaMemcpyAsync(&sl, h->kp.slots + (level % 3), sizeof(Slot), cudaMemcpyDeviceToHost, s));
+  RB_CUDA_TRY(cudaStreamSynchronize(s));
+  if (h_counters) {
+    h_counters[0] = (int64_t)sl.n_next;
+    h_counters[1] = (int64_t)sl.deg_next;
+    h_counters[2] = (int64_t)sl.maxdeg;
+    h_counters[3] = (int64_t)sl.scanned;
+  }
+  if (d_next_local) {
+    const int64_t r = (level + 1) % 3;
+    *d_next_local = r == 0 ? h->kp.fb0 : (r == 1 ? h->kp.fb1 : h->kp.fb2);
+  }
+  return RB_OK;
+}
+
+extern "C" int rb_bfs_words(rb_bfs* h, int64_t* n_words_local, int64_t* n_words_glob) {
+  if (!h) return RB_ERR_ARG;
+  if (n_words_local) *n_words_local = h->n_words;
+  if (n_words_glob) *n_words_glob = h->kp.n_words_glob;
+  return RB_OK;
+}
+
+extern "C" int rb_make_nz(const uint32_t* d_words, int64_t n_words, uint32_t* d_nz, void* stream) {
+  if (n_words % 32) {
+    rb_set_error("rb_make_nz: n_words must be a multiple of 32");
+    return RB_ERR_ARG;
+  }
+  make_nz<<<256, 256, 0, (cudaStream_t)stream>>>(d_words, d_nz, n_words / 32);
+  RB_CUDA_TRY(cudaGetLastError());
   return RB_OK;
 }

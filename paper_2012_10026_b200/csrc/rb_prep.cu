@@ -794,3 +794,67 @@ extern "C" int rb_degree_sort_adjacency(const int64_t* d_rs, const int32_t* d_co
   RB_CUDA_TRY(cudaStreamSynchronize(s));
   return RB_OK;
 }
+
+// ---------------------------------------------------------------------------
+// transpose slice of a 1D partition: for every global u, its owned neighbours
+
+namespace {
+__global__ void transpose_keys(const int64_t* __restrict__ rs, const int32_t* __restrict__ col, int64_t n_local,
+                               int64_t v_lo, uint64_t* __restrict__ keys) {
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int64_t w = warp; w < n_local; w += nwarps) {
+    const int64_t s = rs[w], e = rs[w + 1];
+    const uint64_t owner = (uint64_t)(v_lo + w);
+    for (int64_t j = s + lane; j < e; j += 32) keys[j] = ((uint64_t)(uint32_t)col[j] << 32) | owner;
+  }
+}
+
+size_t transpose_ws(int64_t m_local, uint64_t** A, uint64_t** B, void* base, size_t cap, void** temp,
+                    size_t* temp_bytes) {
+  Carver c(base, cap);
+  *A = c.take<uint64_t>((size_t)std::max<int64_t>(m_local, 1));
+  *B = c.take<uint64_t>((size_t)std::max<int64_t>(m_local, 1));
+  size_t t = 0;
+  cub::DoubleBuffer<uint64_t> db(*A, *B);
+  cub::DeviceRadixSort::SortKeys(nullptr, t, db, std::max<int64_t>(m_local, 1), 0, 64);
+  *temp_bytes = t;
+  *temp = c.take<char>(t);
+  return c.off + 256;
+}
+}  // namespace
+
+extern "C" size_t rb_transpose_workspace_bytes(int64_t m_local, int64_t n_glob) {
+  uint64_t *A, *B;
+  void* temp;
+  size_t tb;
+  (void)n_glob;
+  return transpose_ws(m_local, &A, &B, nullptr, SIZE_MAX, &temp, &tb);
+}
+
+extern "C" int rb_transpose_rows(const int64_t* d_rs, const int32_t* d_col, int64_t n_local, int64_t v_lo,
+                                 int64_t m_local, int64_t n_glob, void* d_ws, size_t ws_bytes, int64_t* d_td_rs,
+                                 int32_t* d_td_col, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  uint64_t *A, *B;
+  void* temp;
+  size_t tb;
+  if (transpose_ws(m_local, &A, &B, d_ws, ws_bytes, &temp, &tb) > ws_bytes) {
+    rb_set_error("rb_transpose_rows: workspace too small");
+    return RB_ERR_ARG;
+  }
+  if (m_local == 0) {
+    RB_CUDA_TRY(cudaMemsetAsync(d_td_rs, 0, (size_t)(n_glob + 1) * 8, s));
+    return RB_OK;
+  }
+  transpose_keys<<<grid_for(n_local * 32), 256, 0, s>>>(d_rs, d_col, n_local, v_lo, A);
+  RB_CUDA_TRY(cudaGetLastError());
+  cub::DoubleBuffer<uint64_t> db(A, B);
+  const int end_bit = 32 + std::max(1, bits_for((uint64_t)(n_glob > 0 ? n_glob - 1 : 0)));
+  size_t t = tb;
+  RB_CUDA_TRY(cub::DeviceRadixSort::SortKeys(temp, t, db, m_local, 0, end_bit, s));
+  csr_emit<<<grid_for(m_local + 1), 256, 0, s>>>(db.Current(), m_local, n_glob, d_td_rs, d_td_col);
+  RB_CUDA_TRY(cudaGetLastError());
+  return RB_OK;
+}
