@@ -47,7 +47,10 @@
 
 namespace {
 
-constexpr int kThreads = 1024;
+#ifndef RB_THREADS
+#define RB_THREADS 1024
+#endif
+constexpr int kThreads = RB_THREADS;
 #ifndef RB_MINB
 #define RB_MINB 1
 #endif
@@ -320,14 +323,16 @@ __device__ __forceinline__ void warp_push_slices(QEnt* hq, unsigned long long* c
 }
 
 // Top-down phase A: the frontier rows straight from the bitmap.  Two-level
-// walk: the lanes of a warp check 32 words of the nonzero summary (each covers
-// 32 bitmap words) strided over the whole range; inside a
-// nonzero summary word the set bits are enumerated across the lanes (prefix
-// sum + n-th set bit), 4 rows per lane per round.  Rows with deg <= 2 claim
-// their inline neighbours directly, rows with deg <= 32 are edge-balanced
-// across the warp (4 edges per lane per step), hub rows are appended as
-// 256-edge slices for phase B.
-__device__ void td_rows(const TdCtx& c, const uint32_t* nzcur, QEnt* hq, unsigned long long* hq_count, Acc& acc) {
+// walk: the lanes of a warp check 32 bytes of the nonzero summary (each bit
+// covers one bitmap word) strided over the whole range; a nonzero item (8
+// words = 256 vertices) is compacted into the warp's shared-memory list (lane
+// l owns byte l of the item: popc + warp scan + a loop over its set bits),
+// then read back 4 rows per lane per round.  Rows with deg <= 2 claim their
+// inline neighbours directly, rows with deg <= 32 are edge-balanced across
+// the warp (4 edges per lane per step), hub rows are appended as 256-edge
+// slices for phase B.
+__device__ void td_rows(const TdCtx& c, const uint32_t* nzcur, QEnt* hq, unsigned long long* hq_count, Acc& acc,
+                        uint32_t* lst) {
   const KParams& p = *c.p;
   const uint32_t lane = rb::lane_id();
   const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
@@ -344,11 +349,20 @@ __device__ void td_rows(const TdCtx& c, const uint32_t* nzcur, QEnt* hq, unsigne
       const uint32_t il = __ffs(mask) - 1;
       const uint64_t wbase = (i0 + (uint64_t)il * nwarps) * 8;  // first bitmap word of this item
       const uint32_t bits = __shfl_sync(RB_FULL, nzb, il);
-      const uint32_t x = (lane < 8 && ((bits >> lane) & 1u)) ? __ldcg(c.fcur + wbase + lane) : 0u;
-      const uint32_t cnt = __popc(x);
+      const uint32_t wi = lane >> 2;
+      const uint32_t x = ((bits >> wi) & 1u) ? __ldcg(c.fcur + wbase + wi) : 0u;
+      uint32_t byte = (x >> (8 * (lane & 3))) & 0xffu;
+      const uint32_t cnt = __popc(byte);
       const uint32_t incl = rb::warp_incl_scan(cnt);
       const uint32_t tot = __shfl_sync(RB_FULL, incl, 31);
-      const uint32_t excl = incl - cnt;
+      uint32_t pos = incl - cnt;
+      const uint32_t vb = (uint32_t)(wbase * 32) + lane * 8;
+      __syncwarp();
+      while (byte) {
+        lst[pos++] = vb + (__ffs(byte) - 1);
+        byte &= byte - 1;
+      }
+      __syncwarp();
       for (uint32_t r = 0; r < tot; r += 32 * kUB) {
         int32_t v[kUB];
         int64_t s0[kUB];
@@ -359,10 +373,7 @@ __device__ void td_rows(const TdCtx& c, const uint32_t* nzcur, QEnt* hq, unsigne
         for (int k = 0; k < kUB; ++k) {
           const uint32_t t = r + 32 * k + lane;
           on[k] = t < tot;
-          const uint32_t o = rb::warp_upper_bound(incl, on[k] ? t : tot - 1);
-          const uint32_t xo = __shfl_sync(RB_FULL, x, o);
-          const uint32_t eo = __shfl_sync(RB_FULL, excl, o);
-          v[k] = (int32_t)((wbase + o) * 32 + nth_set_bit(xo, (on[k] ? t : tot - 1) - eo));
+          v[k] = on[k] ? (int32_t)lst[t] : 0;
           s0[k] = 0;
           d[k] = 0;
           n0[k] = n1[k] = 0;
@@ -743,7 +754,7 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
       c.nznext = nz_of(p, r1);
       c.probe = 2 * mu < p.m_directed;  // fewer than half the edge ends unvisited
       // phase A: frontier rows from the bitmap; hub rows become slices in hq
-      td_rows(c, p.nzcur_ext ? p.nzcur_ext : nz_of(p, r0), hq, &in->hq_count, acc);
+      td_rows(c, p.nzcur_ext ? p.nzcur_ext : nz_of(p, r0), hq, &in->hq_count, acc, s_bu_pair[threadIdx.x >> 5]);
       if (hubs) {  // phase B only if some frontier row has more than kLightDeg edges
         {
           const unsigned long long* const src[1] = {&in->hq_count};
