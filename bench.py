@@ -60,18 +60,20 @@ def hmean(x):
 
 
 def algorithmic_bytes(levels, n_dev: int, n_plus_dev: int) -> int:
-    """TD level: |F|*(4 queue + 16 offsets) + 4*E_TD + n_next*(4 parent + 4 queue + 4 level)
-    BU level: 3*(n_dev/8) + 8*U + 4*C + n_next*(4 parent + 4 level)."""
+    """SURVEY.md 8(d) byte model without its per-vertex level term (the engine,
+    like the reference, keeps no level array unless asked to):
+    TD level: |F|*(4 queue + 16 offsets) + 4*E_TD + n_next*(4 parent + 4 queue)
+    BU level: 3*(n_dev/8) + 8*U + 4*C + n_next*(4 parent)."""
     total = 0
     reached = 0
     for i, r in enumerate(levels):
         reached += r.n_f
         n_next = levels[i + 1].n_f if i + 1 < len(levels) else 0
         if r.direction == "top_down":
-            total += r.n_f * 20 + 4 * r.scanned_edges + n_next * 12
+            total += r.n_f * 20 + 4 * r.scanned_edges + n_next * 8
         else:
             U = max(n_plus_dev - reached, 0)
-            total += 3 * (n_dev // 8) + 8 * U + 4 * r.scanned_edges + n_next * 8
+            total += 3 * (n_dev // 8) + 8 * U + 4 * r.scanned_edges + n_next * 4
     return int(total)
 
 

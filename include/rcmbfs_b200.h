@@ -88,6 +88,10 @@ typedef struct {
   int32_t bu_reverse; /* scan bottom-up rows from their end */
   int64_t n_policy;   /* g.n incl. isolated (engine.py:593) */
   int64_t m_directed; /* g.m_directed */
+  int32_t record_levels; /* also keep a per-vertex level array (not part of
+                            the reference's BfsResult; costs 4 B per reached
+                            vertex in the traversal); 0 = parents only */
+  int32_t reserved0;
 } rb_bfs_params;
 
 /* d_col_bu may equal d_col.  n_dev: vertices [0,n_dev) live on the device

@@ -33,7 +33,7 @@ class LevelRecordC(ctypes.Structure):
 class BfsParamsC(ctypes.Structure):
     _fields_ = [
         ("alpha", I32), ("beta", I32), ("hybrid", I32), ("bu_reverse", I32),
-        ("n_policy", I64), ("m_directed", I64),
+        ("n_policy", I64), ("m_directed", I64), ("record_levels", I32), ("reserved0", I32),
     ]
 
 

@@ -253,7 +253,7 @@ __device__ __forceinline__ void td_claim(const TdCtx& c, const int32_t (&v)[KU],
   for (int k = 0; k < KU; ++k) {
     if (!claim[k]) continue;
     p.parent[wl[k]] = v[k];
-    p.level[wl[k]] = (int32_t)(c.L + 1);
+    if (p.level) p.level[wl[k]] = (int32_t)(c.L + 1);
     const uint32_t old = atomicOr(c.fnext + (wl[k] >> 5), 1u << (wl[k] & 31));
     if (old == 0u) atomicOr(c.nznext + (wl[k] >> 10), 1u << ((wl[k] >> 5) & 31));
   }
@@ -570,7 +570,7 @@ __device__ void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uint
       if (par >= 0) {
         foundm |= 1u << k;
         p.parent[vbase + 32 * k] = par;
-        p.level[vbase + 32 * k] = (int32_t)(L + 1);
+        if (p.level) p.level[vbase + 32 * k] = (int32_t)(L + 1);
         acc.n += 1;
         acc.deg += dg[k];
         acc.maxdeg = max(acc.maxdeg, dg[k]);
@@ -643,7 +643,7 @@ __device__ void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uint
         if (mine && par >= 0) {
           const int64_t v = (int64_t)w0 * 32 + idx;
           p.parent[v] = par;
-          p.level[v] = (int32_t)(L + 1);
+          if (p.level) p.level[v] = (int32_t)(L + 1);
           acc.n += 1;
           acc.deg += d;
           acc.maxdeg = max(acc.maxdeg, d);
@@ -834,7 +834,7 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
 __global__ void bfs_seed(KParams p, int64_t src) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   p.parent[src] = (int32_t)src;
-  p.level[src] = 0;
+  if (p.level) p.level[src] = 0;
   p.fb0[src >> 5] |= 1u << (src & 31);
   p.nz0[src >> 10] |= 1u << ((src >> 5) & 31);
   p.vis[src >> 5] |= 1u << (src & 31);
@@ -997,7 +997,7 @@ extern "C" int rb_bfs_create_part(const int64_t* d_row_starts, const int32_t* d_
 
   RB_ALLOC(k.parent, (size_t)n_dev * 4);
   RB_ALLOC(h->hot, (size_t)n_dev * sizeof(int2));
-  RB_ALLOC(k.level, (size_t)n_dev * 4);
+  if (params->record_levels) RB_ALLOC(k.level, (size_t)n_dev * 4);
   RB_ALLOC(k.slots, 3 * sizeof(Slot));
   RB_ALLOC(k.bar, 64);
   RB_ALLOC(k.rec, kRecCap * sizeof(rb_level_record));
@@ -1096,7 +1096,7 @@ static int reset_common(rb_bfs* h, cudaStream_t s) {
   KParams& k = h->kp;
   const size_t wb = (size_t)h->n_words * 4;
   RB_CUDA_TRY(cudaMemsetAsync(k.parent, 0xff, (size_t)h->n_dev * 4, s));
-  RB_CUDA_TRY(cudaMemsetAsync(k.level, 0xff, (size_t)h->n_dev * 4, s));
+  if (k.level) RB_CUDA_TRY(cudaMemsetAsync(k.level, 0xff, (size_t)h->n_dev * 4, s));
   RB_CUDA_TRY(cudaMemsetAsync(k.fb0, 0, wb, s));
   RB_CUDA_TRY(cudaMemsetAsync(k.fb1, 0, wb, s));
   RB_CUDA_TRY(cudaMemsetAsync(k.nz0, 0, (size_t)h->n_full * 4, s));
@@ -1162,6 +1162,10 @@ extern "C" int rb_bfs_traverse(rb_bfs* h, void* stream) {
 extern "C" int rb_bfs_results(rb_bfs* h, int32_t* parent_out, int32_t* level_out, rb_level_record* h_records,
                               int64_t cap, int64_t* n_records, void* stream) {
   if (!h) return RB_ERR_ARG;
+  if (level_out && !h->kp.level) {
+    rb_set_error("rb_bfs_results: engine created without record_levels");
+    return RB_ERR_ARG;
+  }
   cudaStream_t s = (cudaStream_t)stream;
   if (h->launched) {
     // drain: copy records, continue very deep traversals

@@ -170,7 +170,8 @@ class PartitionedBfs:
 class GpuLocalLevel:
     """The local step of one rank: an rb_bfs engine created with a partition."""
 
-    def __init__(self, g, bounds: list[int], rank: int, alpha: int, beta: int, hybrid: bool = True):
+    def __init__(self, g, bounds: list[int], rank: int, alpha: int, beta: int, hybrid: bool = True,
+                 record_levels: bool = False):
         torch = _lib.require_cuda()
         self.torch = torch
         self.device = torch.device("cuda", torch.cuda.current_device())
@@ -207,7 +208,7 @@ class GpuLocalLevel:
         flags[:n_local] = (self.deg_local == 0).to(torch.int64)
         words = (flags.view(nw, 32) << torch.arange(32, device=self.device, dtype=torch.int64)).sum(dim=1)
         self.iso = torch.where(words >= (1 << 31), words - (1 << 32), words).to(torch.int32)
-        prm = _lib.BfsParamsC(alpha, beta, int(hybrid), 1, g.n, g.m_directed)
+        prm = _lib.BfsParamsC(alpha, beta, int(hybrid), 1, g.n, g.m_directed, int(record_levels), 0)
         part = _lib.PartitionC(lo, n_glob, _lib.ptr(self.td_rs).value, _lib.ptr(self.td_col).value)
         self.h = ctypes.c_void_p(0)
         _lib.check(L.rb_bfs_create_part(_lib.ptr(self.rs_local), _lib.ptr(self.col_local), _lib.ptr(self.col_local),

@@ -194,9 +194,10 @@ class _DeviceBfs:
     """Owns one rb_bfs handle: graph views + device traversal state."""
 
     def __init__(self, g: CsrGraph, *, hybrid: bool, alpha: int, beta: int, g_bu: CsrGraph | None,
-                 bu_reverse: bool, trim_isolated: bool):
+                 bu_reverse: bool, trim_isolated: bool, record_levels: bool = False):
         torch = _lib.require_cuda()
         self.torch = torch
+        self.record_levels = record_levels
         L = _lib.lib()
         self.g = g
         rs, col, deg = g.device_arrays()
@@ -224,7 +225,7 @@ class _DeviceBfs:
         if g_bu is not None:
             col_bu = g_bu.device_arrays()[1]
             self._keep.append(col_bu)
-        prm = _lib.BfsParamsC(alpha, beta, int(hybrid), int(bu_reverse), n, g.m_directed)
+        prm = _lib.BfsParamsC(alpha, beta, int(hybrid), int(bu_reverse), n, g.m_directed, int(record_levels), 0)
         _lib.check(
             L.rb_bfs_create(_lib.ptr(rs), _lib.ptr(col), _lib.ptr(col_bu), _lib.ptr(deg), n_dev,
                             _lib.ptr(iso) if iso is not None else None, ctypes.byref(prm), ctypes.byref(self.h)),
@@ -297,7 +298,11 @@ def _records_to_levels(recs) -> list:
 class BfsEngine:
     """Reusable traversal context (engine.py:478-604): device state per graph."""
 
-    def __init__(self, g: CsrGraph, params: BfsParams, g_desc: CsrGraph | None = None):
+    def __init__(self, g: CsrGraph, params: BfsParams, g_desc: CsrGraph | None = None, *,
+                 record_levels: bool = False):
+        """``record_levels`` (an extension, not in the reference) also keeps a
+        per-vertex level array on the device (``level_device``); it costs one
+        extra 4-byte write per reached vertex inside the traversal."""
         self.g = g
         self.params = params
         self.g_desc = g_desc
@@ -315,7 +320,7 @@ class BfsEngine:
         reduced = params.mode == "hybrid_reduced"
         self._dev = _DeviceBfs(
             g, hybrid=hybrid, alpha=params.alpha, beta=params.beta, g_bu=g_desc if reduced else None,
-            bu_reverse=not reduced, trim_isolated=True,
+            bu_reverse=not reduced, trim_isolated=True, record_levels=record_levels,
         )
         self._deg_dev = g.device_arrays()[2]
 
@@ -372,6 +377,8 @@ class BfsEngine:
         return _ptr_view(_lib.lib().rb_bfs_parent_ptr(self._dev.h), self._dev.n_dev)
 
     def level_device(self):
+        if not self._dev.record_levels:
+            raise ValueError("engine created without record_levels=True")
         return _ptr_view(_lib.lib().rb_bfs_level_ptr(self._dev.h), self._dev.n_dev)
 
 

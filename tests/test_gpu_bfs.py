@@ -48,7 +48,7 @@ def test_levels_and_records_vs_reference(cuda_ok, golden_kron, ocache, key):
     g2 = c["g2"]
     labels = oracle.csr_components(g2)
     g = to_rb(g2)
-    with rb.BfsEngine(g, rb.BfsParams(mode="hybrid")) as eng:
+    with rb.BfsEngine(g, rb.BfsParams(mode="hybrid"), record_levels=True) as eng:
         assert eng.n_dev == c["n_plus"]  # isolated tail dropped
         for r in ref["roots"]:
             res = eng.run(r["source"])
@@ -64,7 +64,7 @@ def test_modes_agree(cuda_ok, ocache):
     labels = oracle.csr_components(g2)
     g, gd = to_rb(g2), desc_of(g2)
     srcs = oracle.sample_sources(g2.degrees, 8, 7)
-    engines = {m: rb.BfsEngine(g, rb.BfsParams(mode=m), g_desc=gd) for m in rb.MODES}
+    engines = {m: rb.BfsEngine(g, rb.BfsParams(mode=m), g_desc=gd, record_levels=True) for m in rb.MODES}
     try:
         for s in srcs:
             s = int(s)
@@ -167,7 +167,7 @@ def test_hubs_split_across_warps(cuda_ok):
     labels = oracle.csr_components(g_or)
     g = to_rb(g_or)
     for mode in ("hybrid", "level_sync"):
-        with rb.BfsEngine(g, rb.BfsParams(mode=mode)) as eng:
+        with rb.BfsEngine(g, rb.BfsParams(mode=mode), record_levels=True) as eng:
             for s in (hub_a, hub_b, int(la[0]), int(extra[0, 0])):
                 _, want, _, _ = oracle.seq_bfs(g_or, s)
                 res = eng.run(s)
@@ -182,6 +182,8 @@ def test_engine_reuse_is_deterministic_in_levels(cuda_ok, ocache):
         a = eng.run(5)
         b = eng.run(7)
         c = eng.run(5)
+        with pytest.raises(ValueError, match="record_levels"):
+            eng.level_device()  # per-vertex levels are opt-in
     la = [r.n_f for r in a.levels]
     assert la == [r.n_f for r in c.levels]
     assert np.array_equal(a.predecessor >= 0, c.predecessor >= 0)

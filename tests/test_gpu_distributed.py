@@ -44,7 +44,7 @@ def _run_ranks(rank, world, backend, port, scale, align, q):
     dist.init_process_group(backend, rank=rank, world_size=world, **kw)
     g2, n_plus = _graph(scale, 1)
     bounds = partition_bounds(g2.row_starts, n_plus, world, align)
-    local = GpuLocalLevel(g2, bounds, rank, alpha=64, beta=8)
+    local = GpuLocalLevel(g2, bounds, rank, alpha=64, beta=8, record_levels=True)
     drv = PartitionedBfs(local, bounds, rank, world, n_policy=g2.n, m_directed=g2.m_directed)
     roots = rb.sample_sources(g2.degrees, 6, 3)
     out = []
