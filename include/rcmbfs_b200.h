@@ -157,6 +157,23 @@ int rb_bfs_barrier_probe(rb_bfs* h, int iters, double* ns_per_barrier, void* str
  * after the grid barrier, 0. */
 int rb_bfs_debug_timestamps(rb_bfs* h, uint64_t* out, int64_t cap, int* blocks);
 
+/* ---- tree validation (validate.py:63-225) ----------- */
+/* Component labels = min vertex id of the component (validate.py:63-84),
+ * by device union-find over the raw edge list d_edges (m_raw pairs, may hold
+ * duplicates / self loops) or, if d_edges is NULL, over the CSR. */
+int rb_components(const int64_t* d_row_starts, const int32_t* d_col, int64_t n, const uint32_t* d_edges,
+                  int64_t m_raw, int32_t* d_labels, void* stream);
+size_t rb_validate_workspace_bytes(int64_t n);
+/* The five rules of Validator.validate (validate.py:123-225) for one
+ * predecessor array.  d_levels receives the derived levels (-1 unreached or
+ * unresolved).  h_first_bad[5]: per rule -1 if it passed, else the first
+ * counterexample the reference reports -- rule 1: the source; 2: vertex
+ * (out-of-range parents take precedence); 3: vertex; 4: CSR edge index;
+ * 5: vertex.  RB_ERR_ARG if source is out of range. */
+int rb_validate(const int64_t* d_row_starts, const int32_t* d_col, int64_t n, const int32_t* d_labels,
+                int64_t source, const int32_t* d_parent, void* d_ws, size_t ws_bytes, int32_t* d_levels,
+                int64_t* h_first_bad, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -482,10 +482,10 @@ EXPORT int or_validate(int64_t n, const int64_t* rs, const uint32_t* dst, const 
     if (parent[v] < 0 || levels[v] >= 0) continue;
     int64_t sp = 0, u = v, bad = 0;
     while (levels[u] < 0) {
-      if (sp > n || parent[u] < 0 || parent[u] >= n) { bad = 1; break; }
+      /* a chain longer than n vertices is a cycle */
+      if (sp >= n || parent[u] < 0 || parent[u] >= n) { bad = 1; break; }
       stack[sp++] = u;
       u = parent[u];
-      if (sp > n) { bad = 1; break; }
     }
     if (bad) { ok[2] = 0; continue; }
     int64_t base = levels[u];

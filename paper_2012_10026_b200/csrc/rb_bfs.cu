@@ -8,35 +8,42 @@
 // block from the same device counters, so no host round trip happens between
 // levels.
 //
-// State (HBM; n_dev = non-isolated prefix of the RCM graph):
-//   vis[]        uint32 words: vertices of levels < L (+ isolated, padding)
+// State (HBM; n_dev = non-isolated prefix of the RCM graph, word arrays
+// padded to whole 8192-vertex tiles):
+//   vis[]        uint32 words: every discovered vertex (+ isolated, padding)
 //   fb[3][]      frontier bitmaps, rotated: fcur = fb[L%3], fnext = fb[(L+1)%3];
 //                fb[(L+2)%3] is zeroed during level L (it is fnext of L+1)
-//   lq[2]        light frontier vertices (deg <= kLightDeg), int32
-//   hq[2]        hub work items (chunk << 32 | v): one entry per kChunk-edge
-//                slice of a hub row, so hubs spread over many warps
-//   parent, level  int32 per vertex
+//   nz[3][]      one bit per bitmap word: "word nonzero" (rotated with fb)
+//   hq[2]        hub slices {row offset, vertex, length}: one 16-B entry per
+//                256-edge slice of a frontier row longer than 32
+//   vinfo[]      32-B row record {row start, degree, first two neighbours}
+//   hot[]        int2 per vertex: the first two neighbours in bottom-up order
+//   parent[]     int32; level[] only when the caller asks for it
 // Invariant: vis holds every vertex discovered so far (the current frontier
-// included), so a top-down claim is one atomicOr on vis and a bottom-up
-// step tests ~vis directly.
+// included), so a top-down claim is one atomicOr on vis and a bottom-up step
+// tests ~vis directly.
 //
 // The path is latency-bound integer work, so both directions are written for
 // memory-level parallelism: every lane keeps several independent loads in
-// flight (unrolled edge / vertex groups), work items are sized so the whole
-// grid is busy, and there is no per-item atomic work fetching.
+// flight, work items are dealt statically so the whole grid is busy, and
+// there is no per-item atomic work fetching.
 //
-// Top-down: warps take items statically (light batches of 32 rows that are
-// edge-balanced with a warp prefix sum, processed 128 edges per step; or one
-// 256-edge hub slice, 8 edges per lane).  A neighbour is claimed with one
-// atomicOr on its visited word; the winner sets the next-frontier bit (RED),
-// writes parent / level and appends to the next queue (warp-aggregated).
-// Bottom-up: a warp owns kUB consecutive bitmap words (kUB*32 vertices), so
-// its visited / next-frontier words are written with plain stores.  Each lane
-// checks its unvisited vertices' rows from the scan start kK1 neighbours at a
-// time (reverse row order by default: RCM ids ascend with degree, so the end
-// of a row holds the likely frontier hubs), continuing up to kK2 checks;
-// longer rows are finished by the whole warp 256 neighbours per step with a
-// ballot early exit.
+// Top-down (phase A, td_rows): warps walk the nonzero summary of the frontier
+// bitmap; each nonzero 256-vertex item is compacted into a per-warp
+// shared-memory list and its rows' records are loaded 4 per lane.  Rows of
+// degree <= 2 claim the neighbours held in the record, rows of degree <= 32
+// are edge-balanced across the warp, longer rows are appended as 256-edge
+// slices that every warp shares after a grid barrier (phase B, td_hubs).  A
+// neighbour is claimed with one atomicOr on its visited word; the winner sets
+// the next-frontier bit, the nonzero-summary bit and the parent.
+// Bottom-up (bu_level): a warp owns kBU = 8 consecutive bitmap words (256
+// vertices), lane l bit l of each, so visited / next-frontier words are
+// written with plain stores.  Round 1 checks the two scan-first neighbours
+// from hot[] (reverse row order by default: RCM ids ascend with degree, so
+// the end of a row holds the likely frontier hubs); rows still open are
+// compacted across the warp and continued 8 neighbours per lane per step up
+// to kK2 checks; longer rows are finished by the whole warp 256 neighbours
+// per step with a ballot early exit.
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -57,13 +64,11 @@ constexpr int kThreads = RB_THREADS;
 constexpr int kWarps = kThreads / 32;
 constexpr uint32_t kLightDeg = 32;  // deg <= kLightDeg -> light queue
 constexpr uint32_t kTinyDeg = 2;    // deg <= kTinyDeg -> tiny queue (neighbours inline)
-constexpr int kTinyPerLane = 4;     // tiny rows per lane per top-down item
 constexpr int kChunkPerLane = 8;
 constexpr uint32_t kChunk = 32 * kChunkPerLane;  // edges per hub work item
 constexpr int kTdUnroll = 4;                     // light batch: edges per lane per step
 constexpr int kUB = 4;                           // compaction: words per warp step
 constexpr int kBU = 8;                           // bottom-up: words per warp step
-constexpr int kK1 = 2;                           // bottom-up: first-round checks per vertex
 constexpr int kK2 = 258;                         // bottom-up: per-lane checks before the warp takes over
 constexpr int kHeavyPerLane = 8;                 // warp-cooperative bottom-up: neighbours per lane per step
 constexpr int64_t kRecCap = 4096;                // level records per launch
@@ -207,16 +212,6 @@ __device__ __forceinline__ void ld_vinfo(const VInfo* q, int64_t& s, uint32_t& d
   d = (uint32_t)a.z;
   n0 = a.w;
   n1 = b.x;
-}
-
-__device__ __forceinline__ uint32_t nth_set_bit(uint32_t x, uint32_t k) {  // 0-based, LSB first
-  uint32_t pos = 0, c;
-  c = __popc(x & 0xffffu); if (k >= c) { k -= c; x >>= 16; pos += 16; }
-  c = __popc(x & 0xffu);   if (k >= c) { k -= c; x >>= 8;  pos += 8; }
-  c = __popc(x & 0xfu);    if (k >= c) { k -= c; x >>= 4;  pos += 4; }
-  c = __popc(x & 0x3u);    if (k >= c) { k -= c; x >>= 2;  pos += 2; }
-  c = x & 1u;              if (k >= c) { pos += 1; }
-  return pos;
 }
 
 // Warp-collective claim of KU edges per lane (v[k] -> w[k], act[k]).

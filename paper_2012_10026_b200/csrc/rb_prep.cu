@@ -59,7 +59,6 @@ struct Carver {  // carve a caller workspace into aligned pieces
     off = o + count * sizeof(T);
     return base ? (T*)(base + o) : nullptr;
   }
-  bool ok() const { return off <= cap; }
 };
 
 int grid_for(int64_t n, int threads = 256) {

@@ -84,3 +84,20 @@ def cuda_ok():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return True
+
+
+@pytest.fixture(scope="session")
+def golden_validate():
+    arr = dict(np.load(os.path.join(GOLDEN, "validate.npz")))
+    with open(os.path.join(GOLDEN, "validate_details.json")) as f:
+        details = json.load(f)
+    return arr, details
+
+
+def validate_cases(golden):
+    """Yield (n, edges, source, parent, checks, levels, details) per reference case."""
+    arr, details = golden
+    for i in range(int(arr["n_cases"][0])):
+        gi, src = (int(x) for x in arr[f"c{i}_graph"])
+        yield (int(arr[f"g{gi}_n"][0]), arr[f"g{gi}_edges"], src, arr[f"c{i}_parent"], arr[f"c{i}_checks"].tolist(),
+               arr[f"c{i}_levels"], details[i])

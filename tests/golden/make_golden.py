@@ -18,6 +18,9 @@ Contents
                      level-array sha256, hybrid LevelRecord tuples
                      (direction, n_f, m_f, m_u), traversed edges, raw pairs
 * kron12_perm.npy -- full RCM permutation of Kronecker scale 12 seed 1
+* validate.npz    -- the reference Validator on random graphs with randomly
+                     corrupted trees (cycles, phantom edges, dropped and
+                     foreign vertices): check vector, details, derived levels
 """
 
 from __future__ import annotations
@@ -173,8 +176,52 @@ def kron_fixtures(plan):
     return out
 
 
+def validate_fixtures():
+    """Reference Validator (validate.py:123-225) on corrupted predecessor arrays."""
+    rng = np.random.default_rng(2024)
+    arrays = {}
+    details = []
+    i = 0
+    for gi in range(12):
+        n = int(rng.integers(8, 700))
+        e = rng.integers(0, n, size=(int(n * rng.choice([0.6, 1.2, 3.0])), 2), dtype=np.uint32)
+        g = build_csr(EdgeList(n_declared=n, edges=e))
+        val = Validator(g)
+        src = int(rng.integers(0, n))
+        base = bfs_sequential(g, src).predecessor.astype(np.int32)
+        arrays[f"g{gi}_n"] = np.array([n])
+        arrays[f"g{gi}_edges"] = e
+        for t in range(6):
+            bad = base.copy()
+            if t == 1:  # 2-cycle between reached neighbours
+                reach = np.flatnonzero(base >= 0)
+                for a in reach:
+                    nb = [int(w) for w in g.neighbors(int(a)) if int(w) != src and base[w] >= 0]
+                    if int(a) != src and nb:
+                        bad[a], bad[nb[0]] = nb[0], a
+                        break
+            elif t >= 2:
+                k = int(rng.integers(1, 4))
+                idx = rng.integers(0, n, size=k)
+                bad[idx] = rng.integers(-1, n, size=k)
+            rep = val.validate(src, bad)
+            arrays[f"c{i}_graph"] = np.array([gi, src])
+            arrays[f"c{i}_parent"] = bad
+            arrays[f"c{i}_checks"] = np.array([c.passed for c in rep.checks])
+            arrays[f"c{i}_levels"] = rep.derived_levels.astype(np.int64)
+            details.append([c.detail for c in rep.checks])
+            i += 1
+    arrays["n_cases"] = np.array([i])
+    np.savez_compressed(os.path.join(HERE, "validate.npz"), **arrays)
+    with open(os.path.join(HERE, "validate_details.json"), "w") as f:
+        json.dump(details, f, indent=0)
+    print("validate", i, flush=True)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["gen", "small", "kron"]
+    which = sys.argv[1:] or ["gen", "small", "kron", "validate"]
+    if "validate" in which:
+        validate_fixtures()
     if "gen" in which:
         gen_fixtures()
     if "small" in which:
