@@ -30,6 +30,15 @@ int rb_version(void);
 int rb_kronecker_generate(int scale, int64_t edgefactor, uint64_t seed, double a, double b, double c,
                           uint32_t* d_edges, void* stream);
 
+/* Chung-Lu power-law graph (BASELINE configs[4]; no reference generator --
+ * recipe in paper_2012_10026_b200/generator.py).  d_weights: n positive
+ * int64 integer weights; writes m_pairs (u,v) uint32 pairs, each endpoint
+ * drawn with probability weight / total from Philox4x64-10 streams keyed
+ * (seed, 2^32 + chunk).  Workspace: rb_chunglu_workspace_bytes(n). */
+size_t rb_chunglu_workspace_bytes(int64_t n);
+int rb_chunglu_generate(const int64_t* d_weights, int64_t n, int64_t m_pairs, uint64_t seed, void* d_ws,
+                        size_t ws_bytes, uint32_t* d_edges, void* stream);
+
 /* ---- CSR build: replaces graph.py:85-120 (build_csr) -------------------- */
 /* Stage 1 (sizes + error check).  d_edges: m_raw (u,v) uint32 pairs.
  * On an out-of-range edge returns RB_ERR_ARG with *bad_index = first index.

@@ -276,6 +276,39 @@ def kronecker_generate(scale: int, edgefactor: int = 16, initiator=(0.57, 0.19, 
     return n, out
 
 
+def _mulhi64(x: np.ndarray, t: int) -> np.ndarray:
+    """floor(x * t / 2^64) for uint64 x, exact (32-bit limbs)."""
+    m32 = np.uint64(0xFFFFFFFF)
+    s32 = np.uint64(32)
+    xl, xh = x & m32, x >> s32
+    tl, th = np.uint64(t & 0xFFFFFFFF), np.uint64(t >> 32)
+    p0, p1, p2, p3 = xl * tl, xl * th, xh * tl, xh * th
+    mid = (p0 >> s32) + (p1 & m32) + (p2 & m32)
+    return p3 + (p1 >> s32) + (p2 >> s32) + (mid >> s32)
+
+
+def chunglu_generate(n: int, avg_degree: int = 20, gamma: float = 2.1, w_min: float = 1.0, cap_frac: float = 0.01,
+                     seed: int = 7):
+    """(n, edges uint32 (m,2)): numpy restatement of the Chung-Lu recipe
+    (BASELINE configs[4]; no reference generator exists -- the recipe is
+    stated in paper_2012_10026_b200/generator.py::ChungLuParams)."""
+    rng = np.random.Generator(np.random.Philox(key=np.array([seed, (1 << 32) - 1], dtype=np.uint64)))
+    u = rng.random(n)
+    cap = float(max(1, int(cap_frac * n)))
+    w = np.minimum(cap, w_min * (1.0 - u) ** (-1.0 / (gamma - 1.0)))
+    prefix = np.cumsum(np.floor(w * 1024.0).astype(np.int64))
+    total = int(prefix[-1])
+    m = n * avg_degree // 2
+    out = np.empty((m, 2), dtype=np.uint32)
+    for chunk, lo in enumerate(range(0, m, CHUNK_EDGES)):
+        hi = min(lo + CHUNK_EDGES, m)
+        bg = np.random.Philox(key=np.array([seed, (1 << 32) + chunk], dtype=np.uint64))
+        raw = bg.random_raw(2 * (hi - lo)).astype(np.uint64)
+        r = _mulhi64(raw, total).astype(np.int64)
+        out[lo:hi] = np.searchsorted(prefix, r, side="right").reshape(-1, 2).astype(np.uint32)
+    return n, out
+
+
 def sample_sources(degrees: np.ndarray, rounds: int, seed: int) -> np.ndarray:
     """bench.py:124-134."""
     eligible = np.flatnonzero(np.asarray(degrees) > 0)

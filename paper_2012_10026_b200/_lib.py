@@ -75,6 +75,8 @@ _SIGS = {
     "rb_bfs_barrier_probe": ([P, ctypes.c_int, ctypes.POINTER(ctypes.c_double), P], ctypes.c_int),
     "rb_bfs_debug_timestamps": ([P, P, I64, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "rb_components": ([P, P, I64, P, I64, P, P], ctypes.c_int),
+    "rb_chunglu_workspace_bytes": ([I64], SZ),
+    "rb_chunglu_generate": ([P, I64, I64, ctypes.c_uint64, P, SZ, P, P], ctypes.c_int),
     "rb_validate_workspace_bytes": ([I64], SZ),
     "rb_validate": ([P, P, I64, P, I64, P, P, SZ, P, P, P], ctypes.c_int),
 }

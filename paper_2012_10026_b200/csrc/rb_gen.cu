@@ -14,6 +14,8 @@
 // One thread per edge: scale/4 Philox blocks, all arithmetic in registers.
 #include <stdint.h>
 
+#include <cub/cub.cuh>
+
 #include "rb_common.cuh"
 #include "rb_error.h"
 
@@ -87,6 +89,38 @@ __global__ void kron_kernel(GenParams g, uint2* __restrict__ out) {
   }
 }
 
+// Chung-Lu endpoint sampling (BASELINE configs[4]; recipe in generator.py):
+// pair j takes raw words 2i, 2i+1 (i = j mod 65536) of the Philox stream
+// keyed (seed, 2^32 + j / 65536) -- numpy's Philox(key=[seed, 2^32 + c])
+// .random_raw() order -- maps each to r = floor(x * T / 2^64) over the total
+// integer weight T, and picks the first vertex whose inclusive weight prefix
+// exceeds r.  All integer: byte-identical with the numpy restatement.
+__global__ void chunglu_kernel(const int64_t* __restrict__ prefix, int64_t n, int64_t m, uint64_t seed,
+                               uint2* __restrict__ out) {
+  const uint64_t T = (uint64_t)prefix[n - 1];
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t chunk = (1ull << 32) + (uint64_t)(j / kChunkEdges);
+    const int64_t i = j % kChunkEdges;
+    uint64_t words[4] = {(uint64_t)((2 * i) >> 2) + 1, 0, 0, 0};  // words 2i, 2i+1 share one block
+    philox4x64_10(words, seed, chunk);
+    uint32_t ends[2];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const uint64_t r = __umul64hi(words[(2 * i + t) & 3], T);
+      int64_t lo = 0, hi = n - 1;  // first idx with prefix[idx] > r (exists: r < T)
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((uint64_t)__ldg(prefix + mid) > r)
+          hi = mid;
+        else
+          lo = mid + 1;
+      }
+      ends[t] = (uint32_t)lo;
+    }
+    out[j] = make_uint2(ends[0], ends[1]);
+  }
+}
+
 uint64_t splitmix64(uint64_t x) {
   x = x + 0x9E3779B97F4A7C15ull;
   uint64_t z = x;
@@ -126,6 +160,31 @@ extern "C" int rb_kronecker_generate(int scale, int64_t edgefactor, uint64_t see
   int64_t blocks = (g.m + 255) / 256;
   if (blocks > 148 * 64) blocks = 148 * 64;
   kron_kernel<<<(int)blocks, 256, 0, s>>>(g, reinterpret_cast<uint2*>(d_edges));
+  RB_CUDA_TRY(cudaGetLastError());
+  return RB_OK;
+}
+
+extern "C" size_t rb_chunglu_workspace_bytes(int64_t n) {
+  size_t t = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, t, (const int64_t*)nullptr, (int64_t*)nullptr, (int)(n > 0 ? n : 1));
+  return (size_t)(n > 0 ? n : 1) * 8 + 256 + t;
+}
+
+extern "C" int rb_chunglu_generate(const int64_t* d_weights, int64_t n, int64_t m_pairs, uint64_t seed, void* d_ws,
+                                   size_t ws_bytes, uint32_t* d_edges, void* stream) {
+  if (n < 1 || n >= (1ll << 31) || m_pairs < 0 || !d_weights || !d_edges || ws_bytes < rb_chunglu_workspace_bytes(n)) {
+    rb_set_error("rb_chunglu_generate: invalid argument");
+    return RB_ERR_ARG;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t* prefix = reinterpret_cast<int64_t*>(d_ws);
+  void* temp = reinterpret_cast<char*>(d_ws) + (((size_t)n * 8 + 255) & ~(size_t)255);
+  size_t t = ws_bytes - (((size_t)n * 8 + 255) & ~(size_t)255);
+  RB_CUDA_TRY(cub::DeviceScan::InclusiveSum(temp, t, d_weights, prefix, (int)n, s));
+  if (m_pairs == 0) return RB_OK;
+  int64_t blocks = (m_pairs + 255) / 256;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  chunglu_kernel<<<(int)blocks, 256, 0, s>>>(prefix, n, m_pairs, seed, reinterpret_cast<uint2*>(d_edges));
   RB_CUDA_TRY(cudaGetLastError());
   return RB_OK;
 }
