@@ -39,15 +39,31 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=64)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--graph", default="kronecker", choices=["kronecker", "chunglu"],
+                    help="kronecker (configs[0..3]) or chunglu (configs[4]: n=2^24, gamma 2.1, seed 7)")
     ap.add_argument("--scale", type=int, default=22)
     ap.add_argument("--edgefactor", type=int, default=16)
-    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--seed", type=int, default=None, help="default: 1 (kronecker), 7 (chunglu)")
     ap.add_argument("--mode", default="hybrid")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-roots", type=int, default=0, help="only run N roots (for ncu)")
-    return ap.parse_args()
+    ap.add_argument("--validate-roots", type=int, default=64,
+                    help="validate this many of the timed roots' trees on the GPU (outside the timed region)")
+    a = ap.parse_args()
+    if a.seed is None:
+        a.seed = 7 if a.graph == "chunglu" else 1
+    return a
+
+
+def workload(args):
+    """(config.workload name, data description) of the graph being measured."""
+    if args.graph == "chunglu":
+        return (f"chunglu-n2^{args.scale}-g2.1-d20-rcm-bfs",
+                f"synthetic Chung-Lu power law (generator.py ChungLuParams recipe, seed {args.seed})")
+    return (f"kronecker-s{args.scale}-ef{args.edgefactor}-rcm-bfs",
+            f"synthetic Kronecker (reference generator, seed {args.seed})")
 
 
 def hmean(x):
@@ -131,10 +147,11 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
-def load_traffic():
+def load_traffic(name: str):
+    """ncu dram bytes per bfs_persistent launch for this workload (profiles/roofline_traffic.json)."""
     try:
         with open(os.path.join(ROOT, "profiles", "roofline_traffic.json")) as f:
-            return json.load(f)
+            return json.load(f).get(name)
     except Exception:
         return None
 
@@ -143,11 +160,14 @@ def load_traffic():
 # CPU reference arm (oracle port of BfsEngine hybrid, all host cores)
 
 
-def cpu_graph(scale, edgefactor, seed):
+def cpu_graph(args):
     import oracle
 
     t0 = time.perf_counter()
-    n, e = oracle.kronecker_generate(scale, edgefactor, seed=seed)
+    if args.graph == "chunglu":
+        n, e = oracle.chunglu_generate(1 << args.scale, seed=args.seed)
+    else:
+        n, e = oracle.kronecker_generate(args.scale, args.edgefactor, seed=args.seed)
     t1 = time.perf_counter()
     g = oracle.build_csr(n, e)
     t2 = time.perf_counter()
@@ -199,7 +219,7 @@ def run_reference(args):
 
     oracle.build()
     threads = os.cpu_count() or 1
-    cg = cpu_graph(args.scale, args.edgefactor, args.seed)
+    cg = cpu_graph(args)
     roots = oracle.sample_sources(cg["g2"].degrees, 64, 1)
     raw = raw_pairs_for(cg["ranges"], cg["inv"], cg["edges"], roots)
     for s in roots[: args.warmup]:
@@ -216,11 +236,11 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": k,
         "warmup": args.warmup, "ms_per_step": 1e3 * wall / k, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "int32", "data": "synthetic Kronecker (reference generator, seed 1)",
-        "config": {"workload": f"kronecker-s{args.scale}-ef{args.edgefactor}-rcm-bfs", "scale": args.scale,
+        "vs_baseline": None, "dtype": "int32", "data": workload(args)[1],
+        "config": {"workload": workload(args)[0], "scale": args.scale,
                    "edgefactor": args.edgefactor, "roots": k, "mode": "hybrid"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{k} seeded roots of the scale-{args.scale} RCM graph, oracle C port of "
+                         "sample": f"{k} seeded roots of the {workload(args)[0]} graph, oracle C port of "
                                    f"BfsEngine hybrid (td_plain + bu_range), OpenMP {threads} threads"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "preprocessing_s": cg["timings"],
@@ -255,8 +275,11 @@ def run_ours(args):
 
     # ---- preprocessing (timed separately, reported, not part of the metric)
     t0 = time.perf_counter()
-    el = rb.kronecker_generate(rb.KroneckerParams(scale=args.scale, edgefactor=args.edgefactor, seed=args.seed),
-                               device=True)
+    if args.graph == "chunglu":
+        el = rb.chunglu_generate(rb.ChungLuParams(n=1 << args.scale, seed=args.seed), device=True)
+    else:
+        el = rb.kronecker_generate(rb.KroneckerParams(scale=args.scale, edgefactor=args.edgefactor, seed=args.seed),
+                                   device=True)
     torch.cuda.synchronize()
     t_gen = time.perf_counter() - t0
     torch.cuda.synchronize()
@@ -335,6 +358,19 @@ def run_ours(args):
         e2e_teps.append(raw[j] / dt)
     d2h = 4 * n_dev + 64 * len(res.levels)
 
+    # ---- tree validation on the GPU (validate.py rules), outside the timed region
+    n_val, n_ok = 0, 0
+    if args.validate_roots > 0:
+        val = rb.Validator(g2)
+        full = torch.full((g2.n,), -1, dtype=torch.int32, device="cuda")
+        for j in my[: args.validate_roots]:
+            eng.run_device(int(roots[j]))
+            full[:n_dev] = eng.parent_device()
+            bad, _, _ = val.validate_device(int(roots[j]), full)
+            n_val += 1
+            n_ok += int((bad < 0).all())
+        del val, full
+
     value_rank = hmean(teps) / 1e9
     ms_rank = 1e3 * float(np.mean(times))
     if dist is not None:
@@ -355,14 +391,12 @@ def run_ours(args):
 
     peak, peak_kind = measured_peak()
     ach = float(np.sum(bytes_alg) / np.sum(times) / 1e9)
-    traffic = load_traffic()
-    if traffic is not None and f"-s{args.scale}-" not in traffic.get("config", "").replace("kronecker-s", "-s"):
-        traffic = None  # the committed ncu capture is for another scale
+    traffic = load_traffic(workload(args)[0])
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": len(my), "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
-        "data": "synthetic Kronecker (reference generator, seed 1), built on device",
-        "config": {"workload": f"kronecker-s{args.scale}-ef{args.edgefactor}-rcm-bfs", "scale": args.scale,
+        "data": workload(args)[1] + ", built on device",
+        "config": {"workload": workload(args)[0], "scale": args.scale,
                    "edgefactor": args.edgefactor, "roots": len(my), "mode": args.mode,
                    "parallelism": "replicas" if world > 1 else "single",
                    "l2": "flushed (256 MiB write) before every root", "n": int(g2.n), "n_plus": int(n_plus_dev),
@@ -378,6 +412,8 @@ def run_ours(args):
                      "traffic": None if traffic is None else traffic.get("bytes_per_launch")},
         "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": 8, "d2h_bytes_per_step": int(d2h),
                 "api": "BfsEngine.run(source) -> BfsResult with host predecessor"},
+        "validation": {"roots": n_val, "passed": n_ok,
+                       "method": "GPU Validator: the 5 rules of validate.py (tree edges, levels, spans, coverage)"},
         "gpu_launches": int(len(my) * 2),  # bfs_seed + bfs_persistent per root
         "clocks": clk.summary(),
         "timed_wall_ms": wall_ms,
@@ -466,8 +502,8 @@ def run_partitioned(args, rb, torch, dist, g2, stats, roots, raw, world, rank, p
             "metric": METRIC, "value": hmean(teps) / 1e9, "unit": UNIT, "n_gpus": world, "steps": len(my),
             "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int32",
-            "data": "synthetic Kronecker (reference generator, seed 1), built on device",
-            "config": {"workload": f"kronecker-s{args.scale}-ef{args.edgefactor}-rcm-bfs", "scale": args.scale,
+            "data": workload(args)[1] + ", built on device",
+            "config": {"workload": workload(args)[0], "scale": args.scale,
                        "edgefactor": args.edgefactor, "roots": len(my), "mode": args.mode,
                        "parallelism": f"1d-partition x{world} (NCCL all-gather / all-reduce per level)",
                        "partition_bounds": bounds, "l2": "flushed (256 MiB write) before every root"},

@@ -276,6 +276,27 @@ class _DeviceBfs:
         _lib.check(L.rb_bfs_elapsed(self.h, ctypes.byref(el)), "rb_bfs_elapsed")  # all launches of the traversal
         return self._recs[: nrec.value], el.value
 
+    def parents_to_host(self, out: np.ndarray, chunks: int = 4):
+        """Copy the parents [0, n_dev) into ``out`` (int32 numpy, length >= n_dev;
+        the tail is set to -1): pinned-buffer DMA in chunks, each chunk's
+        multi-threaded host copy overlapping the next chunk's transfer."""
+        torch = self.torch
+        n_dev = self.n_dev
+        dev = _ptr_view(_lib.lib().rb_bfs_parent_ptr(self.h), n_dev)
+        pt = torch.from_numpy(out)
+        step = -(-n_dev // chunks)
+        evs = []
+        for a in range(0, n_dev, step):
+            b = min(a + step, n_dev)
+            self.pinned[a:b].copy_(dev[a:b], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            evs.append((a, b, ev))
+        pt[n_dev:].fill_(-1)
+        for a, b, ev in evs:
+            ev.synchronize()
+            pt[a:b].copy_(self.pinned[a:b])
+
     def level_tensor(self):
         """Device int32 level array over [0, n_dev) (valid after results())."""
         ptr = _lib.lib().rb_bfs_level_ptr(self.h)
@@ -322,7 +343,7 @@ class BfsEngine:
             g, hybrid=hybrid, alpha=params.alpha, beta=params.beta, g_bu=g_desc if reduced else None,
             bu_reverse=not reduced, trim_isolated=True, record_levels=record_levels,
         )
-        self._deg_dev = g.device_arrays()[2]
+        self._deg_host = g.degrees  # host copy (once per graph): the per-run isolated-source check
 
     @property
     def n_dev(self) -> int:
@@ -352,12 +373,12 @@ class BfsEngine:
         if not 0 <= source < g.n:
             raise ValueError(f"source {source} out of range for n={g.n}")
         source = int(source)
-        if source >= self._dev.n_dev or int(self._deg_dev[source].item()) == 0:
+        if source >= self._dev.n_dev or int(self._deg_host[source]) == 0:
             return self._trivial(source)
         self._dev.traverse(source)
+        recs, elapsed = self._dev.results(want_parent=False)
         pred = np.empty(g.n, dtype=np.int32)
-        recs, elapsed = self._dev.results(parent_host=pred)  # D2H straight into the result array
-        pred[self._dev.n_dev :] = -1  # dropped isolated tail
+        self._dev.parents_to_host(pred)
         levels = _records_to_levels(recs)
         traversed = sum(r.m_f for r in levels) // 2  # = sum deg[reached] // 2 (engine.py:599-600)
         return BfsResult(source=source, n=g.n, predecessor=pred, levels=levels, elapsed_time=elapsed,
