@@ -67,10 +67,12 @@ constexpr uint32_t kTinyDeg = 2;    // deg <= kTinyDeg -> tiny queue (neighbours
 constexpr int kChunkPerLane = 8;
 constexpr uint32_t kChunk = 32 * kChunkPerLane;  // edges per hub work item
 constexpr int kTdUnroll = 4;                     // light batch: edges per lane per step
-constexpr int kUB = 4;                           // compaction: words per warp step
+constexpr int kUB = 4;                           // top-down: rows per lane per round
+constexpr int64_t kDenseFrontier = 8192;         // top-down: word-granular dealing from this frontier size
 constexpr int kBU = 8;                           // bottom-up: words per warp step
 constexpr int kK2 = 258;                         // bottom-up: per-lane checks before the warp takes over
 constexpr int kHeavyPerLane = 8;                 // warp-cooperative bottom-up: neighbours per lane per step
+constexpr uint64_t kDbgWarpBase = 65536;  // RB_DEBUG_TS buffer: per-block stamps, then per-warp stamps
 constexpr int64_t kRecCap = 4096;                // level records per launch
 
 // Queue entry: a light frontier row (d <= kLightDeg) or one hub slice
@@ -317,27 +319,150 @@ __device__ __forceinline__ void warp_push_slices(QEnt* hq, unsigned long long* c
   }
 }
 
-// Top-down phase A: the frontier rows straight from the bitmap.  Two-level
-// walk: the lanes of a warp check 32 bytes of the nonzero summary (each bit
-// covers one bitmap word) strided over the whole range; a nonzero item (8
-// words = 256 vertices) is compacted into the warp's shared-memory list (lane
-// l owns byte l of the item: popc + warp scan + a loop over its set bits),
-// then read back 4 rows per lane per round.  Rows with deg <= 2 claim their
-// inline neighbours directly, rows with deg <= 32 are edge-balanced across
-// the warp (4 edges per lane per step), hub rows are appended as 256-edge
-// slices for phase B.
-__device__ void td_rows(const TdCtx& c, const uint32_t* nzcur, QEnt* hq, unsigned long long* hq_count, Acc& acc,
-                        uint32_t* lst) {
+// Top-down phase A: the frontier rows straight from the bitmap.  Rows with
+// deg <= 2 claim their inline neighbours directly, rows with deg <= 32 are
+// edge-balanced across the warp (4 edges per lane per step), hub rows are
+// appended as 256-edge slices for phase B.
+// The rows of a warp's shared-memory list lst[0, tot), 4 per lane per round.
+__device__ __forceinline__ void td_list(const TdCtx& c, const uint32_t* lst, uint32_t tot, QEnt* hq,
+                                        unsigned long long* hq_count, Acc& acc) {
+  const KParams& p = *c.p;
+  const uint32_t lane = rb::lane_id();
+  for (uint32_t r = 0; r < tot; r += 32 * kUB) {
+    int32_t v[kUB];
+    int64_t s0[kUB];
+    uint32_t d[kUB];
+    int32_t n0[kUB], n1[kUB];
+    bool on[kUB], hub[kUB];
+#pragma unroll
+    for (int k = 0; k < kUB; ++k) {
+      const uint32_t t = r + 32 * k + lane;
+      on[k] = t < tot;
+      v[k] = on[k] ? (int32_t)lst[t] : 0;
+      s0[k] = 0;
+      d[k] = 0;
+      n0[k] = n1[k] = 0;
+      if (on[k]) ld_vinfo(p.td_vinfo + v[k], s0[k], d[k], n0[k], n1[k]);
+    }
+    // rows with deg <= 2: neighbours are in the record
+    {
+      int32_t tv[2 * kUB], tw[2 * kUB];
+      bool ta[2 * kUB];
+#pragma unroll
+      for (int k = 0; k < kUB; ++k) {
+        const bool tiny = on[k] && d[k] >= 1 && d[k] <= kTinyDeg;
+        tv[2 * k] = tv[2 * k + 1] = v[k];
+        tw[2 * k] = n0[k];
+        tw[2 * k + 1] = n1[k];
+        ta[2 * k] = tiny;
+        ta[2 * k + 1] = tiny && d[k] == 2;
+        hub[k] = on[k] && d[k] > kLightDeg;
+        if (on[k] && !hub[k]) acc.scan += d[k];
+      }
+      td_claim<2 * kUB>(c, tv, tw, ta, acc);
+    }
+    // rows with 2 < deg <= 32: edge-balanced over the warp
+    uint32_t ld[kUB], lsum = 0;
+#pragma unroll
+    for (int k = 0; k < kUB; ++k) {
+      ld[k] = (on[k] && d[k] > kTinyDeg && d[k] <= kLightDeg) ? d[k] : 0u;
+      lsum += ld[k];
+    }
+    const uint32_t li = rb::warp_incl_scan(lsum);
+    const uint32_t lt = __shfl_sync(RB_FULL, li, 31);
+    for (uint32_t base = 0; base < lt; base += 32 * kTdUnroll) {
+      int32_t vv[kTdUnroll], w[kTdUnroll];
+      bool act[kTdUnroll];
+#pragma unroll
+      for (int q = 0; q < kTdUnroll; ++q) {
+        const uint32_t e = base + 32 * q + lane;
+        act[q] = e < lt;
+        const uint32_t ec = act[q] ? e : lt - 1;
+        const uint32_t o = rb::warp_upper_bound(li, ec);
+        uint32_t local = ec - (__shfl_sync(RB_FULL, li, o) - __shfl_sync(RB_FULL, lsum, o));
+        int32_t rv = 0;
+        int64_t rs0 = 0;
+        bool got = false;
+#pragma unroll
+        for (int k = 0; k < kUB; ++k) {
+          const uint32_t dk = __shfl_sync(RB_FULL, ld[k], o);
+          const int32_t vk = __shfl_sync(RB_FULL, v[k], o);
+          const int64_t sk = rb::shfl_i64(s0[k], o);
+          if (!got && local < dk) {
+            got = true;
+            rv = vk;
+            rs0 = sk + local;
+          } else if (!got) {
+            local -= dk;
+          }
+        }
+        vv[q] = rv;
+        w[q] = act[q] ? rb::ldg_i32(p.td_col + rs0) : 0;
+      }
+      td_claim<kTdUnroll>(c, vv, w, act, acc);
+    }
+    warp_push_slices<kUB>(hq, hq_count, v, s0, d, hub);
+  }
+}
+
+// Top-down phase A, dense frontiers: batch q (of Q = nw / 32) holds the
+// bitmap words q + l * Q, one per lane, so consecutive words fall in
+// consecutive batches and a dense region of a clustered (RCM) frontier
+// spreads over every CTA and warp 32 vertices at a time.  CTA b owns batches
+// b, b + gridDim.x, ...; its warps claim them from a shared counter (one
+// batch ahead, its words in flight).  The nonzero words of a batch are
+// compacted into the warp's shared-memory list, at most 256 rows per round
+// (popc + warp scan + a loop over each lane's set bits).
+__device__ void td_rows_words(const TdCtx& c, QEnt* hq, unsigned long long* hq_count, Acc& acc, uint32_t* lst,
+                              uint32_t* s_next) {
+  const KParams& p = *c.p;
+  const uint32_t lane = rb::lane_id();
+  const uint64_t nw = (uint64_t)p.n_words_glob;
+  const uint64_t Q = (nw + 31) / 32;
+  auto claim = [&]() -> uint64_t {
+    uint32_t k = 0;
+    if (lane == 0) k = atomicAdd(s_next, 1u);
+    k = __shfl_sync(RB_FULL, k, 0);
+    return (uint64_t)blockIdx.x + (uint64_t)k * gridDim.x;
+  };
+  uint64_t q_nx = claim();
+  uint64_t w_nx = q_nx + (uint64_t)lane * Q;
+  uint32_t x_nx = (q_nx < Q && w_nx < nw) ? __ldcg(c.fcur + w_nx) : 0u;
+  while (q_nx < Q) {
+    uint32_t x = x_nx;
+    const uint32_t vb = (uint32_t)(w_nx * 32);
+    q_nx = claim();
+    w_nx = q_nx + (uint64_t)lane * Q;
+    x_nx = (q_nx < Q && w_nx < nw) ? __ldcg(c.fcur + w_nx) : 0u;
+    while (__any_sync(RB_FULL, x != 0u)) {
+      // take a prefix of the lanes whose rows fit the 256-entry list
+      const uint32_t cnt = __popc(x);
+      const uint32_t incl = rb::warp_incl_scan(cnt);
+      const bool take = incl <= 32u * kBU;
+      const uint32_t tot = __reduce_max_sync(RB_FULL, take ? incl : 0u);
+      __syncwarp();
+      if (take) {
+        uint32_t pos = incl - cnt;
+        for (uint32_t y = x; y; y &= y - 1) lst[pos++] = vb + (__ffs(y) - 1);
+        x = 0u;
+      }
+      __syncwarp();
+      td_list(c, lst, tot, hq, hq_count, acc);
+    }
+  }
+}
+
+// Top-down phase A, sparse frontiers: the lanes of a warp check 32 bytes of
+// the nonzero summary (each bit covers one bitmap word, a byte one 256-vertex
+// item) strided over the whole range, so one load skips 32 empty items; a
+// nonzero item is compacted into the warp's list (lane l owns byte l).
+__device__ void td_rows_items(const TdCtx& c, const uint32_t* nzcur, QEnt* hq, unsigned long long* hq_count,
+                              Acc& acc, uint32_t* lst) {
   const KParams& p = *c.p;
   const uint32_t lane = rb::lane_id();
   const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
-  const uint64_t gw = warp_slot();
-  // work item = 8 consecutive bitmap words (256 vertices) = one byte of the
-  // nonzero summary.  Lane l of warp g checks item g + (l + 32 i) * nwarps:
-  // one load skips 32 empty items, and the dense regions of a clustered (RCM)
-  // frontier are dealt round-robin over all warps.
   const uint64_t n_items = (uint64_t)p.n_words_glob / 8;
-  for (uint64_t i0 = gw; i0 < n_items; i0 += nwarps * 32) {
+  for (uint64_t i0 = warp_slot(); i0 < n_items; i0 += nwarps * 32) {
     const uint64_t ime = i0 + (uint64_t)lane * nwarps;
     const uint32_t nzb = ime < n_items ? (ld_bits(nzcur + (ime >> 2)) >> (8 * (ime & 3))) & 0xffu : 0u;
     for (uint32_t mask = __ballot_sync(RB_FULL, nzb != 0u); mask; mask &= mask - 1) {
@@ -358,81 +483,7 @@ __device__ void td_rows(const TdCtx& c, const uint32_t* nzcur, QEnt* hq, unsigne
         byte &= byte - 1;
       }
       __syncwarp();
-      for (uint32_t r = 0; r < tot; r += 32 * kUB) {
-        int32_t v[kUB];
-        int64_t s0[kUB];
-        uint32_t d[kUB];
-        int32_t n0[kUB], n1[kUB];
-        bool on[kUB], hub[kUB];
-#pragma unroll
-        for (int k = 0; k < kUB; ++k) {
-          const uint32_t t = r + 32 * k + lane;
-          on[k] = t < tot;
-          v[k] = on[k] ? (int32_t)lst[t] : 0;
-          s0[k] = 0;
-          d[k] = 0;
-          n0[k] = n1[k] = 0;
-          if (on[k]) ld_vinfo(p.td_vinfo + v[k], s0[k], d[k], n0[k], n1[k]);
-        }
-        // rows with deg <= 2: neighbours are in the record
-        {
-          int32_t tv[2 * kUB], tw[2 * kUB];
-          bool ta[2 * kUB];
-#pragma unroll
-          for (int k = 0; k < kUB; ++k) {
-            const bool tiny = on[k] && d[k] >= 1 && d[k] <= kTinyDeg;
-            tv[2 * k] = tv[2 * k + 1] = v[k];
-            tw[2 * k] = n0[k];
-            tw[2 * k + 1] = n1[k];
-            ta[2 * k] = tiny;
-            ta[2 * k + 1] = tiny && d[k] == 2;
-            hub[k] = on[k] && d[k] > kLightDeg;
-            if (on[k] && !hub[k]) acc.scan += d[k];
-          }
-          td_claim<2 * kUB>(c, tv, tw, ta, acc);
-        }
-        // rows with 2 < deg <= 32: edge-balanced over the warp
-        uint32_t ld[kUB], lsum = 0;
-#pragma unroll
-        for (int k = 0; k < kUB; ++k) {
-          ld[k] = (on[k] && d[k] > kTinyDeg && d[k] <= kLightDeg) ? d[k] : 0u;
-          lsum += ld[k];
-        }
-        const uint32_t li = rb::warp_incl_scan(lsum);
-        const uint32_t lt = __shfl_sync(RB_FULL, li, 31);
-        for (uint32_t base = 0; base < lt; base += 32 * kTdUnroll) {
-          int32_t vv[kTdUnroll], w[kTdUnroll];
-          bool act[kTdUnroll];
-#pragma unroll
-          for (int q = 0; q < kTdUnroll; ++q) {
-            const uint32_t e = base + 32 * q + lane;
-            act[q] = e < lt;
-            const uint32_t ec = act[q] ? e : lt - 1;
-            const uint32_t o = rb::warp_upper_bound(li, ec);
-            uint32_t local = ec - (__shfl_sync(RB_FULL, li, o) - __shfl_sync(RB_FULL, lsum, o));
-            int32_t rv = 0;
-            int64_t rs0 = 0;
-            bool got = false;
-#pragma unroll
-            for (int k = 0; k < kUB; ++k) {
-              const uint32_t dk = __shfl_sync(RB_FULL, ld[k], o);
-              const int32_t vk = __shfl_sync(RB_FULL, v[k], o);
-              const int64_t sk = rb::shfl_i64(s0[k], o);
-              if (!got && local < dk) {
-                got = true;
-                rv = vk;
-                rs0 = sk + local;
-              } else if (!got) {
-                local -= dk;
-              }
-            }
-            vv[q] = rv;
-            w[q] = act[q] ? rb::ldg_i32(p.td_col + rs0) : 0;
-          }
-          td_claim<kTdUnroll>(c, vv, w, act, acc);
-        }
-        warp_push_slices<kUB>(hq, hq_count, v, s0, d, hub);
-      }
+      td_list(c, lst, tot, hq, hq_count, acc);
     }
   }
 }
@@ -509,19 +560,27 @@ __device__ __forceinline__ int32_t bu_heavy(const KParams& p, const uint32_t* fc
 
 template <bool kRev>
 __device__ void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uint32_t* fnext, uint32_t* nznext,
-                         Acc& acc, uint32_t* s_found, uint32_t* s_pair) {
+                         Acc& acc, uint32_t* s_found, uint32_t* s_pair, uint32_t* s_next) {
   const uint32_t lane = rb::lane_id();
-  const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
-  const uint64_t gw = warp_slot();
   const uint64_t nw = (uint64_t)p.n_words;
-  const uint64_t stride = nwarps * kBU;
-  // software pipeline: the visited words of the next step are in flight while
-  // this step works (fnext is pre-zeroed, so fully visited words need no store)
-  uint64_t w0 = gw * kBU;
-  uint32_t vw_next = (w0 < nw && lane < kBU) ? __ldcg(p.vis + w0 + lane) : 0xffffffffu;
-  for (; w0 < nw; w0 += stride) {
-    const uint32_t vw = vw_next;
-    vw_next = (w0 + stride < nw && lane < kBU) ? __ldcg(p.vis + w0 + stride + lane) : 0xffffffffu;
+  // CTA b owns the steps b, b + gridDim.x, ... (kBU words each); its warps
+  // take them in order from a shared-memory counter, so a warp that meets
+  // long rows does not hold up the CTA.  Software pipeline: the next step
+  // is claimed and its visited words are in flight while this step works
+  // (fnext is pre-zeroed, so fully visited words need no store).
+  auto claim_step = [&]() -> uint64_t {
+    uint32_t k = 0;
+    if (lane == 0) k = atomicAdd(s_next, 1u);
+    k = __shfl_sync(RB_FULL, k, 0);
+    return ((uint64_t)blockIdx.x + (uint64_t)k * gridDim.x) * kBU;
+  };
+  uint64_t w_nx = claim_step();
+  uint32_t vw_nx = (w_nx < nw && lane < kBU) ? __ldcg(p.vis + w_nx + lane) : 0xffffffffu;
+  while (w_nx < nw) {
+    const uint64_t w0 = w_nx;
+    const uint32_t vw = vw_nx;
+    w_nx = claim_step();
+    vw_nx = (w_nx < nw && lane < kBU) ? __ldcg(p.vis + w_nx + lane) : 0xffffffffu;
     // lane l owns vertex (w0 + k) * 32 + l of each of the kBU words
     uint32_t actm = 0;
 #pragma unroll
@@ -700,6 +759,9 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
   __shared__ unsigned long long s_ctr[4];
   __shared__ uint32_t s_bu_found[kWarps][kBU];
   __shared__ uint32_t s_bu_pair[kWarps][32 * kBU];
+  __shared__ uint32_t s_bu_next[2];  // bottom-up: next step of this CTA (level parity)
+  if (threadIdx.x == 0) s_bu_next[0] = s_bu_next[1] = 0u;
+  __syncthreads();
   const uint32_t nblocks = gridDim.x;
   const uint64_t gtid = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
   const uint64_t gthreads = (uint64_t)nblocks * kThreads;
@@ -737,6 +799,7 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
     for (uint64_t i = gtid; i < (uint64_t)p.n_words / 32; i += gthreads) nzzero[i] = 0u;
     if (blockIdx.x == 0 && threadIdx.x < sizeof(Slot) / 8)
       reinterpret_cast<unsigned long long*>(p.slots + r1)[threadIdx.x] = 0ull;
+    if (threadIdx.x == 0) s_bu_next[(L + 1) & 1] = 0u;  // the next level's counter (idle during this one)
 
     Acc acc{0, 0, 0, 0u};
     if (dir == 0) {
@@ -749,7 +812,11 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
       c.nznext = nz_of(p, r1);
       c.probe = 2 * mu < p.m_directed;  // fewer than half the edge ends unvisited
       // phase A: frontier rows from the bitmap; hub rows become slices in hq
-      td_rows(c, p.nzcur_ext ? p.nzcur_ext : nz_of(p, r0), hq, &in->hq_count, acc, s_bu_pair[threadIdx.x >> 5]);
+      if (nf >= kDenseFrontier)
+        td_rows_words(c, hq, &in->hq_count, acc, s_bu_pair[threadIdx.x >> 5], &s_bu_next[L & 1]);
+      else
+        td_rows_items(c, p.nzcur_ext ? p.nzcur_ext : nz_of(p, r0), hq, &in->hq_count, acc,
+                      s_bu_pair[threadIdx.x >> 5]);
       if (hubs) {  // phase B only if some frontier row has more than kLightDeg edges
         {
           const unsigned long long* const src[1] = {&in->hq_count};
@@ -760,8 +827,10 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
       }
     } else {
       const uint32_t wib = threadIdx.x >> 5;
-      bu_level<kRev>(p, L, fcur, fnext, nz_of(p, r1), acc, s_bu_found[wib], s_bu_pair[wib]);
+      bu_level<kRev>(p, L, fcur, fnext, nz_of(p, r1), acc, s_bu_found[wib], s_bu_pair[wib], &s_bu_next[L & 1]);
     }
+    if (p.dbg && (threadIdx.x & 31) == 0 && done < 64)  // RB_DEBUG_TS: per-warp end of work
+      p.dbg[kDbgWarpBase + ((uint64_t)done * gridDim.x + blockIdx.x) * kWarps + (threadIdx.x >> 5)] = globaltimer();
     block_add3(s_red, acc, out);
     const uint64_t tB = globaltimer();
     {
@@ -997,7 +1066,7 @@ extern "C" int rb_bfs_create_part(const int64_t* d_row_starts, const int32_t* d_
   RB_ALLOC(k.bar, 64);
   RB_ALLOC(k.rec, kRecCap * sizeof(rb_level_record));
   RB_ALLOC(k.fin, sizeof(Final));
-  if (getenv("RB_DEBUG_TS")) RB_ALLOC(k.dbg, (size_t)64 * 4 * 8 * 1024);
+  if (getenv("RB_DEBUG_TS")) RB_ALLOC(k.dbg, ((size_t)kDbgWarpBase + (size_t)64 * 1024 * kWarps) * 8);
 #undef RB_ALLOC
   if (rc != RB_OK) {
     rb_bfs_destroy(h);
@@ -1256,7 +1325,7 @@ extern "C" int rb_bfs_barrier_probe(rb_bfs* h, int iters, double* ns_per_barrier
 
 extern "C" int rb_bfs_debug_timestamps(rb_bfs* h, uint64_t* out, int64_t cap, int* blocks) {
   if (!h || !h->kp.dbg) return RB_ERR_ARG;
-  const int64_t n = (int64_t)64 * 4 * h->blocks;
+  const int64_t n = (int64_t)kDbgWarpBase + (int64_t)64 * h->blocks * kWarps;  // see kDbgWarpBase
   RB_CUDA_TRY(cudaMemcpy(out, h->kp.dbg, (size_t)(n < cap ? n : cap) * 8, cudaMemcpyDeviceToHost));
   *blocks = h->blocks;
   return RB_OK;
