@@ -69,7 +69,9 @@ constexpr uint32_t kChunk = 32 * kChunkPerLane;  // edges per hub work item
 constexpr int kTdUnroll = 4;                     // light batch: edges per lane per step
 constexpr int kUB = 4;                           // top-down: rows per lane per round
 constexpr int64_t kDenseFrontier = 8192;         // top-down: word-granular dealing from this frontier size
-constexpr int kBU = 8;                           // bottom-up: words per warp step
+constexpr int kBU = 8;                           // bottom-up: max words per warp step (template KB <= kBU)
+constexpr int64_t kSmallGraph = 1ll << 23;       // n_dev up to this: 4-word bottom-up steps (shorter chains)
+constexpr int kList = 256;                       // top-down: rows per warp list round
 constexpr int kK2 = 258;                         // bottom-up: per-lane checks before the warp takes over
 constexpr int kHeavyPerLane = 8;                 // warp-cooperative bottom-up: neighbours per lane per step
 constexpr uint64_t kDbgWarpBase = 65536;  // RB_DEBUG_TS buffer: per-block stamps, then per-warp stamps
@@ -438,7 +440,7 @@ __device__ void td_rows_words(const TdCtx& c, QEnt* hq, unsigned long long* hq_c
       // take a prefix of the lanes whose rows fit the 256-entry list
       const uint32_t cnt = __popc(x);
       const uint32_t incl = rb::warp_incl_scan(cnt);
-      const bool take = incl <= 32u * kBU;
+      const bool take = incl <= (uint32_t)kList;
       const uint32_t tot = __reduce_max_sync(RB_FULL, take ? incl : 0u);
       __syncwarp();
       if (take) {
@@ -558,12 +560,13 @@ __device__ __forceinline__ int32_t bu_heavy(const KParams& p, const uint32_t* fc
   return -1;
 }
 
-template <bool kRev>
+template <bool kRev, int KB>
 __device__ void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uint32_t* fnext, uint32_t* nznext,
                          Acc& acc, uint32_t* s_found, uint32_t* s_pair, uint32_t* s_next) {
   const uint32_t lane = rb::lane_id();
   const uint64_t nw = (uint64_t)p.n_words;
-  // CTA b owns the steps b, b + gridDim.x, ... (kBU words each); its warps
+  int32_t* const level_out = p.level;
+  // CTA b owns the steps b, b + gridDim.x, ... (KB words each); its warps
   // take them in order from a shared-memory counter, so a warp that meets
   // long rows does not hold up the CTA.  Software pipeline: the next step
   // is claimed and its visited words are in flight while this step works
@@ -572,70 +575,72 @@ __device__ void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uint
     uint32_t k = 0;
     if (lane == 0) k = atomicAdd(s_next, 1u);
     k = __shfl_sync(RB_FULL, k, 0);
-    return ((uint64_t)blockIdx.x + (uint64_t)k * gridDim.x) * kBU;
+    return ((uint64_t)blockIdx.x + (uint64_t)k * gridDim.x) * KB;
   };
   uint64_t w_nx = claim_step();
-  uint32_t vw_nx = (w_nx < nw && lane < kBU) ? __ldcg(p.vis + w_nx + lane) : 0xffffffffu;
+  uint32_t vw_nx = (w_nx < nw && lane < KB) ? __ldcg(p.vis + w_nx + lane) : 0xffffffffu;
   while (w_nx < nw) {
     const uint64_t w0 = w_nx;
     const uint32_t vw = vw_nx;
     w_nx = claim_step();
-    vw_nx = (w_nx < nw && lane < kBU) ? __ldcg(p.vis + w_nx + lane) : 0xffffffffu;
-    // lane l owns vertex (w0 + k) * 32 + l of each of the kBU words
+    vw_nx = (w_nx < nw && lane < KB) ? __ldcg(p.vis + w_nx + lane) : 0xffffffffu;
+    // lane l owns vertex (w0 + k) * 32 + l of each of the KB words
     uint32_t actm = 0;
 #pragma unroll
-    for (int k = 0; k < kBU; ++k) actm |= ((~__shfl_sync(RB_FULL, vw, k) >> lane) & 1u) << k;
+    for (int k = 0; k < KB; ++k) actm |= ((~__shfl_sync(RB_FULL, vw, k) >> lane) & 1u) << k;
     if (!__any_sync(RB_FULL, actm != 0)) continue;
     const int64_t vbase = (int64_t)w0 * 32 + lane;
+    const int2* const hot = p.hot + vbase;
+    const int32_t* const deg = p.deg + vbase;
     // round 1: the two scan-first neighbours from the compact `hot` side
-    // array (8 B per vertex, coalesced) -- all kBU loads in flight
-    int2 hv[kBU];
-    uint32_t dg[kBU];
+    // array (8 B per vertex, coalesced) -- all KB loads in flight
+    int2 hv[KB];
+    uint32_t dg[KB];
 #pragma unroll
-    for (int k = 0; k < kBU; ++k) {
+    for (int k = 0; k < KB; ++k) {
       hv[k] = make_int2(-1, -1);
       dg[k] = 0;
       if ((actm >> k) & 1u) {
-        hv[k] = __ldg(p.hot + vbase + 32 * k);
-        dg[k] = (uint32_t)rb::ldg_i32(p.deg + vbase + 32 * k);
+        hv[k] = __ldg(hot + 32 * k);
+        dg[k] = (uint32_t)__ldg(deg + 32 * k);
       }
     }
-    uint32_t hb0[kBU], hb1[kBU];
+    uint32_t hb0[KB], hb1[KB];
 #pragma unroll
-    for (int k = 0; k < kBU; ++k) {
+    for (int k = 0; k < KB; ++k) {
       hb0[k] = hv[k].x >= 0 ? ld_bits(fcur + (hv[k].x >> 5)) : 0u;
       hb1[k] = hv[k].y >= 0 ? ld_bits(fcur + (hv[k].y >> 5)) : 0u;
     }
-    uint32_t foundm = 0, needm = 0, checks = 0;
+    // branch-free resolution, 32-bit step-local counters
+    uint32_t foundm = 0, needm = 0, checks = 0, dsum = 0, dmax = 0;
+    int32_t* const par_out = p.parent + vbase;
 #pragma unroll
-    for (int k = 0; k < kBU; ++k) {
-      if (!((actm >> k) & 1u)) continue;
-      int32_t par = -1;
-      if (hv[k].x >= 0 && ((hb0[k] >> (hv[k].x & 31)) & 1u)) {
-        par = hv[k].x;
-        checks += 1;
-      } else if (hv[k].y >= 0 && ((hb1[k] >> (hv[k].y & 31)) & 1u)) {
-        par = hv[k].y;
-        checks += 2;
-      } else {
-        checks += dg[k] < 2u ? dg[k] : 2u;
-        if (dg[k] > 2u) needm |= 1u << k;
-      }
-      if (par >= 0) {
-        foundm |= 1u << k;
-        p.parent[vbase + 32 * k] = par;
-        if (p.level) p.level[vbase + 32 * k] = (int32_t)(L + 1);
-        acc.n += 1;
-        acc.deg += dg[k];
-        acc.maxdeg = max(acc.maxdeg, dg[k]);
-      }
+    for (int k = 0; k < KB; ++k) {
+      const bool act = (actm >> k) & 1u;
+      const bool h0 = act && hv[k].x >= 0 && ((hb0[k] >> (hv[k].x & 31)) & 1u);
+      const bool h1 = act && !h0 && hv[k].y >= 0 && ((hb1[k] >> (hv[k].y & 31)) & 1u);
+      const bool found = h0 || h1;
+      checks += h0 ? 1u : (h1 ? 2u : (act ? min(dg[k], 2u) : 0u));
+      if (found) par_out[32 * k] = h0 ? hv[k].x : hv[k].y;
+      foundm |= (uint32_t)found << k;
+      needm |= (uint32_t)(act && !found && dg[k] > 2u) << k;
+      dsum += found ? dg[k] : 0u;
+      dmax = max(dmax, found ? dg[k] : 0u);
     }
+    if (foundm && level_out) {
+#pragma unroll
+      for (int k = 0; k < KB; ++k)
+        if ((foundm >> k) & 1u) level_out[vbase + 32 * k] = (int32_t)(L + 1);
+    }
+    acc.n += __popc(foundm);
+    acc.deg += dsum;
+    acc.maxdeg = max(acc.maxdeg, dmax);
     // Longer rows that did not hit: the (lane, k) pairs are compacted across
     // the warp through shared memory so every lane continues one row (up to
     // kK2 checks, 4 per step); rows longer still are finished by the whole warp.
-    uint32_t* fm_s = s_found;  // kBU words: found bits per word
+    uint32_t* fm_s = s_found;  // KB words: found bits per word
 #pragma unroll
-    for (int k = 0; k < kBU; ++k) {
+    for (int k = 0; k < KB; ++k) {
       const uint32_t fm = __ballot_sync(RB_FULL, (foundm >> k) & 1u);
       if (lane == 0) fm_s[k] = fm;
     }
@@ -709,7 +714,7 @@ __device__ void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uint
     // next-frontier words (pre-zeroed) and visited words: the warp owns them
     uint32_t nzmask = 0;
 #pragma unroll
-    for (int k = 0; k < kBU; ++k) {
+    for (int k = 0; k < KB; ++k) {
       const uint32_t fm = fm_s[k];
       nzmask |= (fm != 0u) << k;
       if (lane == (uint32_t)k && fm) {
@@ -753,12 +758,12 @@ __device__ __forceinline__ void block_add3(unsigned long long* red, const Acc& a
   }
 }
 
-template <bool kRev>
+template <bool kRev, int KB>
 __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
   __shared__ unsigned long long s_red[kWarps * 4];
   __shared__ unsigned long long s_ctr[4];
   __shared__ uint32_t s_bu_found[kWarps][kBU];
-  __shared__ uint32_t s_bu_pair[kWarps][32 * kBU];
+  __shared__ uint32_t s_bu_pair[kWarps][32 * kBU > kList ? 32 * kBU : kList];
   __shared__ uint32_t s_bu_next[2];  // bottom-up: next step of this CTA (level parity)
   if (threadIdx.x == 0) s_bu_next[0] = s_bu_next[1] = 0u;
   __syncthreads();
@@ -827,7 +832,7 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
       }
     } else {
       const uint32_t wib = threadIdx.x >> 5;
-      bu_level<kRev>(p, L, fcur, fnext, nz_of(p, r1), acc, s_bu_found[wib], s_bu_pair[wib], &s_bu_next[L & 1]);
+      bu_level<kRev, KB>(p, L, fcur, fnext, nz_of(p, r1), acc, s_bu_found[wib], s_bu_pair[wib], &s_bu_next[L & 1]);
     }
     if (p.dbg && (threadIdx.x & 31) == 0 && done < 64)  // RB_DEBUG_TS: per-warp end of work
       p.dbg[kDbgWarpBase + ((uint64_t)done * gridDim.x + blockIdx.x) * kWarps + (threadIdx.x >> 5)] = globaltimer();
@@ -995,6 +1000,14 @@ struct rb_bfs {
   void* stream;
 };
 
+// The traversal kernel of an engine: scan direction x bottom-up step width.
+static const void* bfs_kernel(const rb_bfs* h) {
+  bool small = h->n_dev <= kSmallGraph;
+  if (const char* env = getenv("RB_KB")) small = atoi(env) == 4;  // tuning override
+  if (h->bu_reverse) return small ? (const void*)bfs_persistent<true, 4> : (const void*)bfs_persistent<true, 8>;
+  return small ? (const void*)bfs_persistent<false, 4> : (const void*)bfs_persistent<false, 8>;
+}
+
 static int alloc_dev(void** p, size_t bytes) {
   cudaError_t e = cudaMalloc(p, bytes ? bytes : 16);
   if (e != cudaSuccess) {
@@ -1124,10 +1137,7 @@ extern "C" int rb_bfs_create_part(const int64_t* d_row_starts, const int32_t* d_
     rb_bfs_destroy(h);
     return RB_ERR_CUDA;
   }
-  if (h->bu_reverse)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, bfs_persistent<true>, kThreads, 0);
-  else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, bfs_persistent<false>, kThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, bfs_kernel(h), kThreads, 0);
   if (nb < 1) nb = 1;
   h->blocks = nb * h->sms;
   *out = h;
@@ -1201,10 +1211,7 @@ static int launch(rb_bfs* h, cudaStream_t s, int64_t level0, int64_t dir0, int64
   kp.m_directed = h->prm.m_directed;
   void* args[] = {&kp};
   cudaError_t e;
-  if (h->bu_reverse)
-    e = cudaLaunchCooperativeKernel((const void*)bfs_persistent<true>, dim3(h->blocks), dim3(kThreads), args, 0, s);
-  else
-    e = cudaLaunchCooperativeKernel((const void*)bfs_persistent<false>, dim3(h->blocks), dim3(kThreads), args, 0, s);
+  e = cudaLaunchCooperativeKernel(bfs_kernel(h), dim3(h->blocks), dim3(kThreads), args, 0, s);
   if (e != cudaSuccess) {
     rb_set_error("cooperative launch failed: %s", cudaGetErrorString(e));
     return RB_ERR_CUDA;
@@ -1389,10 +1396,7 @@ extern "C" int rb_bfs_dist_level(rb_bfs* h, int64_t level, int direction, int hu
   kp.hubs0 = hubs ? 1 : 0;
   void* args[] = {&kp};
   cudaError_t e;
-  if (h->bu_reverse)
-    e = cudaLaunchCooperativeKernel((const void*)bfs_persistent<true>, dim3(h->blocks), dim3(kThreads), args, 0, s);
-  else
-    e = cudaLaunchCooperativeKernel((const void*)bfs_persistent<false>, dim3(h->blocks), dim3(kThreads), args, 0, s);
+  e = cudaLaunchCooperativeKernel(bfs_kernel(h), dim3(h->blocks), dim3(kThreads), args, 0, s);
   if (e != cudaSuccess) {
     rb_set_error("cooperative launch failed: %s", cudaGetErrorString(e));
     return RB_ERR_CUDA;

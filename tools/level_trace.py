@@ -13,13 +13,17 @@ import paper_2012_10026_b200 as rb  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--scale", type=int, default=22)
+ap.add_argument("--graph", default="kronecker", choices=["kronecker", "chunglu"])
 ap.add_argument("--roots", type=int, default=4)
 ap.add_argument("--mode", default="hybrid")
 ap.add_argument("--brief", action="store_true")
 ap.add_argument("--sources", type=int, nargs="*", default=None)
 ap.add_argument("--flush", action="store_true", help="write 256 MiB before each root (cold L2, like bench.py)")
 a = ap.parse_args()
-el = rb.kronecker_generate(rb.KroneckerParams(scale=a.scale))
+if a.graph == "chunglu":
+    el = rb.chunglu_generate(rb.ChungLuParams(n=1 << a.scale), device=True)
+else:
+    el = rb.kronecker_generate(rb.KroneckerParams(scale=a.scale), device=True)
 g = rb.build_csr(el)
 perm, st = rb.rcm(g)
 g2 = rb.apply_permutation(g, perm)
