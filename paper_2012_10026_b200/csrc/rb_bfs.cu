@@ -156,6 +156,7 @@ struct KParams {
   int64_t need_compact0;
   int64_t max_levels;
   int64_t nf0, mf0, mu0;  // mf0 < 0: derive m_f / m_u from deg(src)
+  int64_t from_fin;       // 1: traversal start; CTA 0 runs the first small levels alone (solo_levels)
   int64_t src;
   int64_t m_directed;
 };
@@ -187,6 +188,10 @@ struct Acc {
 // different SMs, so a small level is not concentrated on a few SMs' LSU/L1.
 __device__ __forceinline__ uint64_t warp_slot() {
   return (uint64_t)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+}
+
+__device__ __forceinline__ void red_or(uint32_t* a, uint32_t v) {
+  asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
 }
 
 struct TdCtx {
@@ -758,6 +763,180 @@ __device__ __forceinline__ void block_add3(unsigned long long* red, const Acc& a
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Solo levels: the first top-down levels of a traversal usually hold a
+// handful of rows (the source, then its neighbours).  A whole-grid level
+// costs a full pass of scans plus a grid barrier (~7 us); CTA 0 instead runs
+// such levels alone with its frontier in shared memory and __syncthreads as
+// the level barrier, while the other CTAs wait at one grid barrier.  The
+// bitmaps end up exactly as the grid path leaves them: claims set the
+// next-frontier bits (+ summary), and the buffer the grid would zero ahead
+// holds exactly the frontier of level L-1, whose bits are cleared from its
+// list.  Entry only at the start of a traversal (level 0, frontier {src}).
+
+constexpr int kSoloCap = 1024;     // frontier vertices held in shared memory
+constexpr int64_t kSoloMf = 4096;  // frontier edges of a solo level
+
+struct SoloShared {
+  unsigned long long deg;  // deg_next
+  unsigned int nn, maxd;   // n_next, max degree of the next frontier
+  unsigned int total;      // edges of the current frontier
+};
+
+// Block-wide exclusive scan of one value per thread (kThreads <= 1024).
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* warp_tot, uint32_t* total) {
+  const uint32_t lane = rb::lane_id(), w = threadIdx.x >> 5;
+  const uint32_t incl = rb::warp_incl_scan(x);
+  if (lane == 31) warp_tot[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    const uint32_t t = lane < (uint32_t)kWarps ? warp_tot[lane] : 0u;
+    const uint32_t ti = rb::warp_incl_scan(t);
+    warp_tot[lane] = ti - t;
+    if (lane == 31) *total = ti;
+  }
+  __syncthreads();
+  return warp_tot[w] + incl - x;
+}
+
+// Runs in CTA 0 only.  On return the state variables describe the first
+// level that is not run solo (or the end of the traversal).
+__device__ __forceinline__ void solo_levels(const KParams& p, uint32_t* smem, SoloShared* sh, uint32_t* warp_tot, int64_t& L,
+                            int& dir, int64_t& nf, int64_t& mf, int64_t& mu, int64_t& done, bool& hubs,
+                            uint64_t& t_prev) {
+  const uint32_t tid = threadIdx.x;
+  uint32_t* qp = smem;                 // frontier of level L-1
+  uint32_t* qc = smem + kSoloCap;      // frontier of level L
+  uint32_t* qn = smem + 2 * kSoloCap;  // frontier of level L+1
+  uint32_t* sOff = smem + 3 * kSoloCap;
+  int64_t* sS = reinterpret_cast<int64_t*>(smem + 4 * kSoloCap);
+  uint32_t np = 0, nc = 1;
+  if (tid == 0) qc[0] = (uint32_t)p.src;
+  __syncthreads();
+  while (true) {
+    const int r0 = (int)(L % 3), r1 = (r0 + 1) % 3, r2 = (r0 + 2) % 3;
+    uint32_t* fnext = fb_of(p, r1);
+    uint32_t* nznext = nz_of(p, r1);
+    uint32_t* fold = fb_of(p, r2);
+    uint32_t* nzold = nz_of(p, r2);
+    if (tid == 0) {
+      sh->nn = 0u;
+      sh->deg = 0ull;
+      sh->maxd = 0u;
+    }
+    if (tid < sizeof(Slot) / 8) reinterpret_cast<unsigned long long*>(p.slots + r1)[tid] = 0ull;
+    // rows of the current frontier
+    uint32_t d = 0;
+    if (tid < nc) {
+      int64_t s0;
+      int32_t n0, n1;
+      ld_vinfo(p.td_vinfo + qc[tid], s0, d, n0, n1);
+      sS[tid] = s0;
+    }
+    const uint32_t off = block_excl_scan(tid < nc ? d : 0u, warp_tot, &sh->total);
+    const uint32_t total = sh->total;
+    if (tid < nc) sOff[tid] = off;
+    __syncthreads();
+    // clear the frontier of level L-1 (the buffer the grid would zero ahead)
+    for (uint32_t i = tid; i < np; i += kThreads) {
+      const uint32_t u = qp[i];
+      atomicAnd(fold + (u >> 5), ~(1u << (u & 31)));
+      atomicAnd(nzold + (u >> 10), ~(1u << ((u >> 5) & 31)));
+    }
+    __syncthreads();
+    // edges, block-balanced: edge e belongs to the last row with sOff <= e
+    const bool probe = 2 * mu < p.m_directed;
+    for (uint32_t e0 = 0; e0 < total; e0 += kThreads) {  // same trip count for every lane
+      const uint32_t e = e0 + tid;
+      bool won = false;
+      int32_t w = 0;
+      uint32_t dw = 0;
+      if (e < total) {
+        uint32_t lo = 0, hi = nc;  // upper_bound(sOff, e) - 1
+        while (hi - lo > 1) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (sOff[mid] <= e)
+            lo = mid;
+          else
+            hi = mid;
+        }
+        const int32_t v = (int32_t)qc[lo];
+        w = rb::ldg_i32(p.td_col + sS[lo] + (e - sOff[lo]));
+        const uint32_t bit = 1u << (w & 31);
+        if (!(probe && (ld_bits(p.vis + (w >> 5)) & bit))) {
+          dw = (uint32_t)rb::ldg_i32(p.deg + w);
+          won = !(atomicOr(p.vis + (w >> 5), bit) & bit);
+          if (won) {
+            p.parent[w] = v;
+            if (p.level) p.level[w] = (int32_t)(L + 1);
+            red_or(fnext + (w >> 5), bit);
+            red_or(nznext + (w >> 10), 1u << ((w >> 5) & 31));
+          }
+        }
+      }
+      // warp-aggregated queue append and counters (one shared atomic per warp)
+      const uint32_t lane = rb::lane_id();
+      const uint32_t wm = __ballot_sync(RB_FULL, won);
+      if (wm) {
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(&sh->nn, (uint32_t)__popc(wm));
+        base = __shfl_sync(RB_FULL, base, 0);
+        const uint32_t pos = base + __popc(wm & ((1u << lane) - 1u));
+        if (won && pos < (uint32_t)kSoloCap) qn[pos] = (uint32_t)w;
+        const unsigned long long ds = rb::warp_sum_u64(won ? dw : 0u);
+        const uint32_t dm = __reduce_max_sync(RB_FULL, won ? dw : 0u);
+        if (lane == 0) {
+          atomicAdd(&sh->deg, ds);
+          atomicMax(&sh->maxd, dm);
+        }
+      }
+    }
+    __syncthreads();
+    // counters, record, policy (engine.py:587-596) -- same as the grid path
+    const int64_t n_next = (int64_t)sh->nn;
+    const int64_t deg_next = (int64_t)sh->deg;
+    hubs = sh->maxd > kLightDeg;
+    if (tid == 32) {
+      const uint64_t t_now = globaltimer();
+      rb_level_record r;
+      r.level = L;
+      r.direction = dir;
+      r.n_f = nf;
+      r.m_f = mf;
+      r.m_u = mu;
+      r.scanned_edges = (int64_t)total;
+      r.t_ns = (int64_t)(t_now - t_prev);
+      r.n_next = n_next;
+      r.t_queue_ns = 0;
+      r.reserved = 0;
+      p.rec[done] = r;
+      t_prev = t_now;
+    }
+    mu -= deg_next;
+    mf = deg_next;
+    nf = n_next;
+    int ndir = 0;
+    if (p.hybrid) {
+      if (dir == 0)
+        ndir = (mf * (int64_t)p.alpha > mu) ? 1 : 0;
+      else
+        ndir = (nf * (int64_t)p.beta < p.n_policy) ? 0 : 1;
+    }
+    dir = ndir;
+    ++L;
+    ++done;
+    __syncthreads();  // everyone has read sh before the next level resets it
+    if (!(nf > 0 && dir == 0 && nf <= kSoloCap && mf <= kSoloMf && done < p.max_levels)) break;
+    uint32_t* t = qp;
+    qp = qc;
+    qc = qn;
+    qn = t;
+    np = nc;
+    nc = (uint32_t)nf;
+  }
+}
+
 template <bool kRev, int KB>
 __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
   __shared__ unsigned long long s_red[kWarps * 4];
@@ -765,6 +944,8 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
   __shared__ uint32_t s_bu_found[kWarps][kBU];
   __shared__ uint32_t s_bu_pair[kWarps][32 * kBU > kList ? 32 * kBU : kList];
   __shared__ uint32_t s_bu_next[2];  // bottom-up: next step of this CTA (level parity)
+  __shared__ SoloShared s_solo;
+  __shared__ uint32_t s_wtot[32];
   if (threadIdx.x == 0) s_bu_next[0] = s_bu_next[1] = 0u;
   __syncthreads();
   const uint32_t nblocks = gridDim.x;
@@ -781,10 +962,39 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
   }
   int64_t done = 0;
   uint32_t epoch = 0;
+  bool solo_hubs = false;
+  if (p.from_fin && mf <= kSoloMf) {
+    // traversal start with a small frontier: CTA 0 runs the first levels
+    // alone, the grid waits at one barrier and picks up the state
+    if (blockIdx.x == 0) {
+      uint64_t t0 = globaltimer();
+      bool h = false;
+      solo_levels(p, &s_bu_pair[0][0], &s_solo, s_wtot, L, dir, nf, mf, mu, done, h, t0);
+      if (threadIdx.x == 0) {
+        p.fin->levels_done = done;
+        p.fin->L = L;
+        p.fin->dir = dir;
+        p.fin->nf = nf;
+        p.fin->mf = mf;
+        p.fin->mu = mu;
+        p.fin->pad = h ? 1 : 0;
+      }
+    }
+    rb::grid_barrier(p.bar, nblocks, epoch);
+    done = (int64_t)rb::ld_relaxed_u64((const unsigned long long*)&p.fin->levels_done);
+    L = (int64_t)rb::ld_relaxed_u64((const unsigned long long*)&p.fin->L);
+    dir = (int)rb::ld_relaxed_u64((const unsigned long long*)&p.fin->dir);
+    nf = (int64_t)rb::ld_relaxed_u64((const unsigned long long*)&p.fin->nf);
+    mf = (int64_t)rb::ld_relaxed_u64((const unsigned long long*)&p.fin->mf);
+    mu = (int64_t)rb::ld_relaxed_u64((const unsigned long long*)&p.fin->mu);
+    solo_hubs = rb::ld_relaxed_u64((const unsigned long long*)&p.fin->pad) != 0;
+    need_compact = dir == 0;
+  }
   int r0 = (int)(L % 3);
   // does the current frontier hold a row longer than kLightDeg?  Level 0: the
   // source's degree; a continuation launch conservatively assumes yes.
   bool hubs = p.hubs0 >= 0 ? p.hubs0 != 0 : ((p.mf0 < 0) ? (mf > (int64_t)kLightDeg) : true);
+  if (p.from_fin && done > 0) hubs = solo_hubs;
   uint64_t t_prev = 0, t_queue = 0;
   if (blockIdx.x == 0 && threadIdx.x == 32) t_prev = globaltimer();
 
@@ -997,6 +1207,7 @@ struct rb_bfs {
   int64_t levels_per_launch;  // kRecCap; RB_LEVELS_PER_LAUNCH=1 gives one launch per level (profiling)
   cudaEvent_t ev_start, ev_end;  // bracket all launches of one traversal
   bool launched;
+  bool solo;  // run the first small levels in one CTA (bfs_solo); RB_SOLO=0 disables
   void* stream;
 };
 
@@ -1037,6 +1248,8 @@ extern "C" int rb_bfs_create_part(const int64_t* d_row_starts, const int32_t* d_
   h->bu_reverse = params->bu_reverse;
   h->launched = false;
   h->levels_per_launch = kRecCap;
+  h->solo = true;
+  if (const char* env = getenv("RB_SOLO")) h->solo = atoi(env) != 0;
   cudaEventCreate(&h->ev_start);
   cudaEventCreate(&h->ev_end);
   if (const char* env = getenv("RB_DEBUG")) h->kp.debug = atoi(env);
@@ -1173,8 +1386,10 @@ static int reset_common(rb_bfs* h, cudaStream_t s) {
   if (k.level) RB_CUDA_TRY(cudaMemsetAsync(k.level, 0xff, (size_t)h->n_dev * 4, s));
   RB_CUDA_TRY(cudaMemsetAsync(k.fb0, 0, wb, s));
   RB_CUDA_TRY(cudaMemsetAsync(k.fb1, 0, wb, s));
+  RB_CUDA_TRY(cudaMemsetAsync(k.fb2, 0, wb, s));  // solo levels rely on all three (see solo_levels)
   RB_CUDA_TRY(cudaMemsetAsync(k.nz0, 0, (size_t)h->n_full * 4, s));
   RB_CUDA_TRY(cudaMemsetAsync(k.nz1, 0, (size_t)h->n_full * 4, s));
+  RB_CUDA_TRY(cudaMemsetAsync(k.nz2, 0, (size_t)h->n_full * 4, s));
   RB_CUDA_TRY(cudaMemsetAsync(k.slots, 0, 3 * sizeof(Slot), s));
   RB_CUDA_TRY(cudaMemsetAsync(k.bar, 0, 64, s));
   return RB_OK;
@@ -1198,7 +1413,7 @@ extern "C" int rb_bfs_reset(rb_bfs* h, int64_t source, void* stream) {
 }
 
 static int launch(rb_bfs* h, cudaStream_t s, int64_t level0, int64_t dir0, int64_t need_compact0, int64_t max_levels,
-                  int64_t nf0, int64_t mf0, int64_t mu0) {
+                  int64_t nf0, int64_t mf0, int64_t mu0, int64_t from_fin = 0) {
   KParams kp = h->kp;
   kp.level0 = level0;
   kp.dir0 = dir0;
@@ -1209,6 +1424,7 @@ static int launch(rb_bfs* h, cudaStream_t s, int64_t level0, int64_t dir0, int64
   kp.mu0 = mu0;
   kp.src = h->source;
   kp.m_directed = h->prm.m_directed;
+  kp.from_fin = from_fin;
   void* args[] = {&kp};
   cudaError_t e;
   e = cudaLaunchCooperativeKernel(bfs_kernel(h), dim3(h->blocks), dim3(kThreads), args, 0, s);
@@ -1224,7 +1440,7 @@ extern "C" int rb_bfs_traverse(rb_bfs* h, void* stream) {
   h->launched = true;
   h->stream = stream;
   RB_CUDA_TRY(cudaEventRecord(h->ev_start, (cudaStream_t)stream));
-  int rc = launch(h, (cudaStream_t)stream, 0, 0, 0, h->levels_per_launch, 1, -1, 0);
+  int rc = launch(h, (cudaStream_t)stream, 0, 0, 0, h->levels_per_launch, 1, -1, 0, h->solo ? 1 : 0);
   if (rc) return rc;
   RB_CUDA_TRY(cudaEventRecord(h->ev_end, (cudaStream_t)stream));
   return RB_OK;
