@@ -132,9 +132,10 @@ int rb_bfs_create_part(const int64_t* d_row_starts, const int32_t* d_col, const 
  * local counters n_next, deg_next, maxdeg, scanned. */
 int rb_bfs_reset_part(rb_bfs* h, int64_t source_global, void* stream);
 int rb_bfs_dist_level(rb_bfs* h, int64_t level, int direction, int hubs, const uint32_t* d_fcur_glob,
-                      const uint32_t* d_nz_glob, uint32_t** d_next_local, int64_t* h_counters, void* stream);
+                      const uint8_t* d_nz_glob, uint32_t** d_next_local, int64_t* h_counters, void* stream);
 int rb_bfs_words(rb_bfs* h, int64_t* n_words_local, int64_t* n_words_glob);
-int rb_make_nz(const uint32_t* d_words, int64_t n_words, uint32_t* d_nz, void* stream);
+/* Nonzero summary of a bitmap: d_nz[i] = (d_words[i] != 0), one byte per word. */
+int rb_make_nz(const uint32_t* d_words, int64_t n_words, uint8_t* d_nz, void* stream);
 /* Transpose slice for a partition: for every global vertex u < n_glob, the
  * owned vertices adjacent to u (ascending). */
 size_t rb_transpose_workspace_bytes(int64_t m_local, int64_t n_glob);

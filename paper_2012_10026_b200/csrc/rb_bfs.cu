@@ -13,7 +13,8 @@
 //   vis[]        uint32 words: every discovered vertex (+ isolated, padding)
 //   fb[3][]      frontier bitmaps, rotated: fcur = fb[L%3], fnext = fb[(L+1)%3];
 //                fb[(L+2)%3] is zeroed during level L (it is fnext of L+1)
-//   nz[3][]      one bit per bitmap word: "word nonzero" (rotated with fb)
+//   nz[3][]      one byte per bitmap word: 1 = "word nonzero" (rotated with fb;
+//                plain byte stores, no atomics)
 //   hq[2]        hub slices {row offset, vertex, length}: one 16-B entry per
 //                256-edge slice of a frontier row longer than 32
 //   vinfo[]      32-B row record {row start, degree, first two neighbours}
@@ -86,13 +87,13 @@ struct __align__(16) QEnt {
   int32_t d;
 };
 
-struct __align__(32) VInfo {  // top-down row record (see ld_vinfo)
-  long long s;
-  int32_t d;
-  int32_t n0;
+struct __align__(16) VInfo {  // top-down row record (see ld_vinfo)
+  uint32_t s_lo;               // row start, low 32 bits
+  uint32_t sd;                 // row start bits 32..39 << 24 | degree (kVdSat: read the row starts)
+  int32_t n0;                  // first two neighbours (-1: none)
   int32_t n1;
-  int32_t pad[3];
 };
+constexpr uint32_t kVdSat = 0xFFFFFFu;
 
 struct Slot {  // per-level counters, triple-buffered by level % 3
   unsigned long long n_next;
@@ -124,9 +125,9 @@ struct KParams {
   uint32_t* fb0;
   uint32_t* fb1;
   uint32_t* fb2;
-  uint32_t* nz0;   // bit i: fb0 word i is nonzero -- lets the queue build skip empty words
-  uint32_t* nz1;
-  uint32_t* nz2;
+  uint8_t* nz0;  // byte i: fb0 word i is nonzero -- lets sparse top-down levels skip empty words
+  uint8_t* nz1;
+  uint8_t* nz2;
   const VInfo* vinfo;  // top-down row records (single GPU: of the graph itself)
   // 1D partition (multi-GPU): this engine owns global vertices [v_lo, v_lo + n_dev);
   // top-down expands every GLOBAL frontier vertex through the transpose slice
@@ -135,9 +136,10 @@ struct KParams {
   int64_t v_lo;
   int64_t n_words_glob;
   const VInfo* td_vinfo;
+  const int64_t* td_rs;  // row starts of the top-down rows (records saturate the degree at 2^24 - 1)
   const int32_t* td_col;
   const uint32_t* fcur_ext;   // if set: the (all-gathered) global frontier bitmap of this level
-  const uint32_t* nzcur_ext;  // and its nonzero summary
+  const uint8_t* nzcur_ext;  // and its nonzero summary (one byte per word)
   int64_t hubs0;              // -1: derive from deg(src); 0 / 1: forced (distributed levels)
   QEnt* hq0;           // hub slices of the current top-down level (alternating)
   QEnt* hq1;
@@ -165,7 +167,7 @@ __device__ __forceinline__ uint32_t* fb_of(const KParams& p, int r) {  // r = le
   return r == 0 ? p.fb0 : (r == 1 ? p.fb1 : p.fb2);
 }
 
-__device__ __forceinline__ uint32_t* nz_of(const KParams& p, int r) {
+__device__ __forceinline__ uint8_t* nz_of(const KParams& p, int r) {
   return r == 0 ? p.nz0 : (r == 1 ? p.nz1 : p.nz2);
 }
 
@@ -199,7 +201,7 @@ struct TdCtx {
   int64_t L;
   const uint32_t* fcur;
   uint32_t* fnext;
-  uint32_t* nznext;
+  uint8_t* nznext;
   bool probe;  // probe visited bits before the atomic (most targets visited)
 };
 
@@ -212,15 +214,17 @@ __device__ __forceinline__ QEnt ld_qent(const QEnt* q) {
   return e;
 }
 
-// Top-down row record: one 32-byte sector per vertex (row start, degree and
-// the first two neighbours), so a scattered frontier costs one sector per row.
-__device__ __forceinline__ void ld_vinfo(const VInfo* q, int64_t& s, uint32_t& d, int32_t& n0, int32_t& n1) {
-  const int4 a = __ldg(reinterpret_cast<const int4*>(q));
-  const int4 b = __ldg(reinterpret_cast<const int4*>(q) + 1);
-  s = (int64_t)(((uint64_t)(uint32_t)a.y << 32) | (uint32_t)a.x);
-  d = (uint32_t)a.z;
-  n0 = a.w;
-  n1 = b.x;
+// Top-down row record: 16 bytes per vertex (row start, degree and the first
+// two neighbours) -- one load per row, two rows per sector in the dense
+// regions of a clustered frontier.
+__device__ __forceinline__ void ld_vinfo(const KParams& p, int64_t v, int64_t& s, uint32_t& d, int32_t& n0,
+                                         int32_t& n1) {
+  const int4 a = __ldg(reinterpret_cast<const int4*>(p.td_vinfo + v));
+  s = (int64_t)(((uint64_t)((uint32_t)a.y >> 24) << 32) | (uint32_t)a.x);
+  d = (uint32_t)a.y & kVdSat;
+  if (d == kVdSat) d = (uint32_t)(rb::ldg_i64(p.td_rs + v + 1) - s);  // degree >= 2^24: rare
+  n0 = a.z;
+  n1 = a.w;
 }
 
 // Warp-collective claim of KU edges per lane (v[k] -> w[k], act[k]).
@@ -258,8 +262,8 @@ __device__ __forceinline__ void td_claim(const TdCtx& c, const int32_t (&v)[KU],
     if (!claim[k]) continue;
     p.parent[wl[k]] = v[k];
     if (p.level) p.level[wl[k]] = (int32_t)(c.L + 1);
-    const uint32_t old = atomicOr(c.fnext + (wl[k] >> 5), 1u << (wl[k] & 31));
-    if (old == 0u) atomicOr(c.nznext + (wl[k] >> 10), 1u << ((wl[k] >> 5) & 31));
+    red_or(c.fnext + (wl[k] >> 5), 1u << (wl[k] & 31));  // fire-and-forget: no return trip
+    c.nznext[wl[k] >> 5] = 1u;
   }
 #pragma unroll
   for (int k = 0; k < KU; ++k) {
@@ -349,7 +353,7 @@ __device__ __forceinline__ void td_list(const TdCtx& c, const uint32_t* lst, uin
       s0[k] = 0;
       d[k] = 0;
       n0[k] = n1[k] = 0;
-      if (on[k]) ld_vinfo(p.td_vinfo + v[k], s0[k], d[k], n0[k], n1[k]);
+      if (on[k]) ld_vinfo(p, v[k], s0[k], d[k], n0[k], n1[k]);
     }
     // rows with deg <= 2: neighbours are in the record
     {
@@ -463,7 +467,7 @@ __device__ void td_rows_words(const TdCtx& c, QEnt* hq, unsigned long long* hq_c
 // the nonzero summary (each bit covers one bitmap word, a byte one 256-vertex
 // item) strided over the whole range, so one load skips 32 empty items; a
 // nonzero item is compacted into the warp's list (lane l owns byte l).
-__device__ void td_rows_items(const TdCtx& c, const uint32_t* nzcur, QEnt* hq, unsigned long long* hq_count,
+__device__ void td_rows_items(const TdCtx& c, const uint8_t* nzcur, QEnt* hq, unsigned long long* hq_count,
                               Acc& acc, uint32_t* lst) {
   const KParams& p = *c.p;
   const uint32_t lane = rb::lane_id();
@@ -471,7 +475,12 @@ __device__ void td_rows_items(const TdCtx& c, const uint32_t* nzcur, QEnt* hq, u
   const uint64_t n_items = (uint64_t)p.n_words_glob / 8;
   for (uint64_t i0 = warp_slot(); i0 < n_items; i0 += nwarps * 32) {
     const uint64_t ime = i0 + (uint64_t)lane * nwarps;
-    const uint32_t nzb = ime < n_items ? (ld_bits(nzcur + (ime >> 2)) >> (8 * (ime & 3))) & 0xffu : 0u;
+    uint32_t nzb = 0u;  // bit j: word 8 * ime + j is nonzero
+    if (ime < n_items) {
+      const uint2 b = __ldcg(reinterpret_cast<const uint2*>(nzcur + ime * 8));
+      nzb = (b.x & 1u) | ((b.x >> 7) & 2u) | ((b.x >> 14) & 4u) | ((b.x >> 21) & 8u) | ((b.y & 1u) << 4) |
+            ((b.y >> 3) & 32u) | ((b.y >> 10) & 64u) | ((b.y >> 17) & 128u);
+    }
     for (uint32_t mask = __ballot_sync(RB_FULL, nzb != 0u); mask; mask &= mask - 1) {
       const uint32_t il = __ffs(mask) - 1;
       const uint64_t wbase = (i0 + (uint64_t)il * nwarps) * 8;  // first bitmap word of this item
@@ -566,7 +575,7 @@ __device__ __forceinline__ int32_t bu_heavy(const KParams& p, const uint32_t* fc
 }
 
 template <bool kRev, int KB>
-__device__ void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uint32_t* fnext, uint32_t* nznext,
+__device__ void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uint32_t* fnext, uint8_t* nznext,
                          Acc& acc, uint32_t* s_found, uint32_t* s_pair, uint32_t* s_next) {
   const uint32_t lane = rb::lane_id();
   const uint64_t nw = (uint64_t)p.n_words;
@@ -716,19 +725,18 @@ __device__ void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uint
       }
       __syncwarp();
     }
-    // next-frontier words (pre-zeroed) and visited words: the warp owns them
-    uint32_t nzmask = 0;
+    // next-frontier words (pre-zeroed), their summary bytes and the visited
+    // words: the warp owns them
 #pragma unroll
     for (int k = 0; k < KB; ++k) {
       const uint32_t fm = fm_s[k];
-      nzmask |= (fm != 0u) << k;
       if (lane == (uint32_t)k && fm) {
         fnext[w0 + k] = fm;
+        nznext[w0 + k] = 1u;
         p.vis[w0 + k] = vw | fm;
       }
     }
     __syncwarp();
-    if (lane == 0 && nzmask) atomicOr(nznext + (w0 >> 5), nzmask << (w0 & 31));
     acc.scan += checks;
   }
 }
@@ -817,9 +825,9 @@ __device__ __forceinline__ void solo_levels(const KParams& p, uint32_t* smem, So
   while (true) {
     const int r0 = (int)(L % 3), r1 = (r0 + 1) % 3, r2 = (r0 + 2) % 3;
     uint32_t* fnext = fb_of(p, r1);
-    uint32_t* nznext = nz_of(p, r1);
+    uint8_t* nznext = nz_of(p, r1);
     uint32_t* fold = fb_of(p, r2);
-    uint32_t* nzold = nz_of(p, r2);
+    uint8_t* nzold = nz_of(p, r2);
     if (tid == 0) {
       sh->nn = 0u;
       sh->deg = 0ull;
@@ -831,7 +839,7 @@ __device__ __forceinline__ void solo_levels(const KParams& p, uint32_t* smem, So
     if (tid < nc) {
       int64_t s0;
       int32_t n0, n1;
-      ld_vinfo(p.td_vinfo + qc[tid], s0, d, n0, n1);
+      ld_vinfo(p, qc[tid], s0, d, n0, n1);
       sS[tid] = s0;
     }
     const uint32_t off = block_excl_scan(tid < nc ? d : 0u, warp_tot, &sh->total);
@@ -842,7 +850,7 @@ __device__ __forceinline__ void solo_levels(const KParams& p, uint32_t* smem, So
     for (uint32_t i = tid; i < np; i += kThreads) {
       const uint32_t u = qp[i];
       atomicAnd(fold + (u >> 5), ~(1u << (u & 31)));
-      atomicAnd(nzold + (u >> 10), ~(1u << ((u >> 5) & 31)));
+      nzold[u >> 5] = 0u;  // the word holds only level L-1 bits: it is zero now
     }
     __syncthreads();
     // edges, block-balanced: edge e belongs to the last row with sOff <= e
@@ -871,7 +879,7 @@ __device__ __forceinline__ void solo_levels(const KParams& p, uint32_t* smem, So
             p.parent[w] = v;
             if (p.level) p.level[w] = (int32_t)(L + 1);
             red_or(fnext + (w >> 5), bit);
-            red_or(nznext + (w >> 10), 1u << ((w >> 5) & 31));
+            nznext[w >> 5] = 1u;
           }
         }
       }
@@ -1006,12 +1014,13 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
     const uint32_t* fcur = p.fcur_ext ? p.fcur_ext : fb_of(p, r0);
     uint32_t* fnext = fb_of(p, r1);
     uint32_t* fzero = fb_of(p, r2);
-    uint32_t* nzzero = nz_of(p, r2);
+    uint8_t* nzzero = nz_of(p, r2);
     // zero ahead: next level's fnext bitmap (+ summary) and the counter slot of level L+1
     const uint64_t tA = globaltimer();
     for (uint64_t i = gtid; i < (uint64_t)p.n_words / 4; i += gthreads)
       reinterpret_cast<uint4*>(fzero)[i] = make_uint4(0u, 0u, 0u, 0u);
-    for (uint64_t i = gtid; i < (uint64_t)p.n_words / 32; i += gthreads) nzzero[i] = 0u;
+    for (uint64_t i = gtid; i < (uint64_t)p.n_words / 16; i += gthreads)
+      reinterpret_cast<uint4*>(nzzero)[i] = make_uint4(0u, 0u, 0u, 0u);
     if (blockIdx.x == 0 && threadIdx.x < sizeof(Slot) / 8)
       reinterpret_cast<unsigned long long*>(p.slots + r1)[threadIdx.x] = 0ull;
     if (threadIdx.x == 0) s_bu_next[(L + 1) & 1] = 0u;  // the next level's counter (idle during this one)
@@ -1115,7 +1124,7 @@ __global__ void bfs_seed(KParams p, int64_t src) {
   p.parent[src] = (int32_t)src;
   if (p.level) p.level[src] = 0;
   p.fb0[src >> 5] |= 1u << (src & 31);
-  p.nz0[src >> 10] |= 1u << ((src >> 5) & 31);
+  p.nz0[src >> 5] = 1u;
   p.vis[src >> 5] |= 1u << (src & 31);
 }
 
@@ -1123,12 +1132,12 @@ __global__ void bfs_seed(KParams p, int64_t src) {
 __global__ void make_vinfo(const int64_t* rs, const int32_t* col, int64_t n, VInfo* vi) {
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s = rs[v], e = rs[v + 1];
+    const uint64_t d = (uint64_t)(e - s);
     VInfo r;
-    r.s = s;
-    r.d = (int32_t)(e - s);
-    r.n0 = e - s > 0 ? col[s] : -1;
-    r.n1 = e - s > 1 ? col[s + 1] : -1;
-    r.pad[0] = r.pad[1] = r.pad[2] = 0;
+    r.s_lo = (uint32_t)s;
+    r.sd = ((uint32_t)((uint64_t)s >> 32) << 24) | (uint32_t)(d < kVdSat ? d : kVdSat);
+    r.n0 = d > 0 ? col[s] : -1;
+    r.n1 = d > 1 ? col[s + 1] : -1;
     vi[v] = r;
   }
 }
@@ -1145,13 +1154,10 @@ __global__ void make_hot(const int64_t* rs, const int32_t* col, int64_t n, int r
   }
 }
 
-// nz[j] bit i <=> words[32*j + i] != 0
-__global__ void make_nz(const uint32_t* words, uint32_t* nz, int64_t n_nz) {
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_nz; j += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t f = 0;
-    for (int i = 0; i < 32; ++i) f |= (words[j * 32 + i] != 0u ? 1u : 0u) << i;
-    nz[j] = f;
-  }
+// nz[i] = words[i] != 0
+__global__ void make_nz(const uint32_t* words, uint8_t* nz, int64_t n_words) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_words; j += (int64_t)gridDim.x * blockDim.x)
+    nz[j] = words[j] != 0u ? 1u : 0u;
 }
 
 // Diagnostics: cost of the grid barrier alone (same grid as the traversal).
@@ -1198,7 +1204,6 @@ struct rb_bfs {
   VInfo* vinfo;
   VInfo* td_vinfo;  // partitioned engines only
   int64_t n_glob;
-  int64_t n_full;  // words of a nonzero-summary bitmap (n_words / 32)
   int blocks;
   int sms;
   int bu_reverse;
@@ -1233,6 +1238,11 @@ extern "C" int rb_bfs_create_part(const int64_t* d_row_starts, const int32_t* d_
                                   const rb_bfs_params* params, const rb_bfs_partition* part, rb_bfs** out) {
   if (!out || !params || n_dev <= 0 || !d_row_starts || !d_col || !d_degrees) {
     rb_set_error("rb_bfs_create: invalid argument");
+    return RB_ERR_ARG;
+  }
+  if (params->m_directed >= (1ll << 40)) {
+    rb_set_error("rb_bfs_create: m_directed %lld exceeds the 40-bit row offsets of the row records",
+                 (long long)params->m_directed);
     return RB_ERR_ARG;
   }
   if (n_dev >= (1ll << 31)) {
@@ -1277,10 +1287,9 @@ extern "C" int rb_bfs_create_part(const int64_t* d_row_starts, const int32_t* d_
   RB_ALLOC(k.fb2, wb);
   RB_ALLOC(h->vis_template, wb);
   RB_ALLOC(h->pad_mask, wb);
-  h->n_full = h->n_words / 32;
-  RB_ALLOC(k.nz0, (size_t)h->n_full * 4);
-  RB_ALLOC(k.nz1, (size_t)h->n_full * 4);
-  RB_ALLOC(k.nz2, (size_t)h->n_full * 4);
+  RB_ALLOC(k.nz0, (size_t)h->n_words);
+  RB_ALLOC(k.nz1, (size_t)h->n_words);
+  RB_ALLOC(k.nz2, (size_t)h->n_words);
   RB_ALLOC(h->vinfo, (size_t)n_dev * sizeof(VInfo));
   RB_ALLOC(k.hq0, nhub * sizeof(QEnt));
   RB_ALLOC(k.hq1, nhub * sizeof(QEnt));
@@ -1320,12 +1329,14 @@ extern "C" int rb_bfs_create_part(const int64_t* d_row_starts, const int32_t* d_
     make_vinfo<<<1024, 256>>>(part->d_td_row_starts, part->d_td_col, part->n_glob, h->td_vinfo);
     k.td_vinfo = h->td_vinfo;
     k.td_col = part->d_td_col;
+    k.td_rs = part->d_td_row_starts;
     h->n_glob = part->n_glob;
   } else {
     k.v_lo = 0;
     k.n_words_glob = h->n_words;
     k.td_vinfo = h->vinfo;
     k.td_col = d_col;
+    k.td_rs = d_row_starts;
     h->n_glob = n_dev;
   }
   if (cudaMemcpy(h->vis_template, h->pad_mask, wb, cudaMemcpyDeviceToDevice) != cudaSuccess) {
@@ -1387,9 +1398,9 @@ static int reset_common(rb_bfs* h, cudaStream_t s) {
   RB_CUDA_TRY(cudaMemsetAsync(k.fb0, 0, wb, s));
   RB_CUDA_TRY(cudaMemsetAsync(k.fb1, 0, wb, s));
   RB_CUDA_TRY(cudaMemsetAsync(k.fb2, 0, wb, s));  // solo levels rely on all three (see solo_levels)
-  RB_CUDA_TRY(cudaMemsetAsync(k.nz0, 0, (size_t)h->n_full * 4, s));
-  RB_CUDA_TRY(cudaMemsetAsync(k.nz1, 0, (size_t)h->n_full * 4, s));
-  RB_CUDA_TRY(cudaMemsetAsync(k.nz2, 0, (size_t)h->n_full * 4, s));
+  RB_CUDA_TRY(cudaMemsetAsync(k.nz0, 0, (size_t)h->n_words, s));
+  RB_CUDA_TRY(cudaMemsetAsync(k.nz1, 0, (size_t)h->n_words, s));
+  RB_CUDA_TRY(cudaMemsetAsync(k.nz2, 0, (size_t)h->n_words, s));
   RB_CUDA_TRY(cudaMemsetAsync(k.slots, 0, 3 * sizeof(Slot), s));
   RB_CUDA_TRY(cudaMemsetAsync(k.bar, 0, 64, s));
   return RB_OK;
@@ -1505,7 +1516,7 @@ extern "C" int rb_bfs_step(rb_bfs* h, int direction, const uint32_t* d_visited_w
   words_or<<<256, 256, 0, s>>>(k.vis, d_visited_words, nw_in);
   words_or<<<256, 256, 0, s>>>(k.vis, d_frontier_words, nw_in);
   RB_CUDA_TRY(cudaMemcpyAsync(k.fb0, d_frontier_words, (size_t)nw_in * 4, cudaMemcpyDeviceToDevice, s));
-  make_nz<<<256, 256, 0, s>>>(k.fb0, k.nz0, h->n_full);
+  make_nz<<<256, 256, 0, s>>>(k.fb0, k.nz0, h->n_words);
   RB_CUDA_TRY(cudaMemcpyAsync(k.parent, d_parent_in, (size_t)h->n_dev * 4, cudaMemcpyDeviceToDevice, s));
   h->source = 0;
   rc = launch(h, s, 0, direction, direction == 0 ? 1 : 0, 1, 1, 0, 0);
@@ -1589,7 +1600,7 @@ extern "C" int rb_bfs_reset_part(rb_bfs* h, int64_t source_global, void* stream)
 }
 
 extern "C" int rb_bfs_dist_level(rb_bfs* h, int64_t level, int direction, int hubs, const uint32_t* d_fcur_glob,
-                                 const uint32_t* d_nz_glob, uint32_t** d_next_local, int64_t* h_counters,
+                                 const uint8_t* d_nz_glob, uint32_t** d_next_local, int64_t* h_counters,
                                  void* stream) {
   if (!h || !d_fcur_glob || !d_nz_glob || (direction != 0 && direction != 1)) {
     rb_set_error("rb_bfs_dist_level: invalid argument");
@@ -1640,12 +1651,12 @@ extern "C" int rb_bfs_words(rb_bfs* h, int64_t* n_words_local, int64_t* n_words_
   return RB_OK;
 }
 
-extern "C" int rb_make_nz(const uint32_t* d_words, int64_t n_words, uint32_t* d_nz, void* stream) {
+extern "C" int rb_make_nz(const uint32_t* d_words, int64_t n_words, uint8_t* d_nz, void* stream) {
   if (n_words % 32) {
     rb_set_error("rb_make_nz: n_words must be a multiple of 32");
     return RB_ERR_ARG;
   }
-  make_nz<<<256, 256, 0, (cudaStream_t)stream>>>(d_words, d_nz, n_words / 32);
+  make_nz<<<256, 256, 0, (cudaStream_t)stream>>>(d_words, d_nz, n_words);
   RB_CUDA_TRY(cudaGetLastError());
   return RB_OK;
 }

@@ -228,7 +228,7 @@ class GpuLocalLevel:
             _lib.check(_lib.lib().rb_bfs_reset_part(self.h, int(source), _lib.stream_ptr()), "rb_bfs_reset_part")
 
     def make_nz(self, glob):
-        nz = self.torch.empty(glob.numel() // 32, dtype=self.torch.int32, device=self.device)
+        nz = self.torch.empty(glob.numel(), dtype=self.torch.uint8, device=self.device)  # one byte per word
         _lib.check(_lib.lib().rb_make_nz(_lib.ptr(glob), glob.numel(), _lib.ptr(nz), _lib.stream_ptr()), "rb_make_nz")
         return nz
 
