@@ -273,7 +273,15 @@ def run_ours(args):
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    # ---- preprocessing (timed separately, reported, not part of the metric)
+    # ---- preprocessing (timed separately, reported, not part of the metric);
+    # one tiny pass first so module loading is not billed to the timings
+    _w = rb.build_csr(rb.kronecker_generate(rb.KroneckerParams(scale=10), device=True))
+    _p, _ = rb.rcm(_w)
+    rb.apply_permutation(_w, _p)
+    if args.graph == "chunglu":
+        rb.chunglu_generate(rb.ChungLuParams(n=1 << 10), device=True)
+    torch.cuda.synchronize()
+    del _w, _p
     t0 = time.perf_counter()
     if args.graph == "chunglu":
         el = rb.chunglu_generate(rb.ChungLuParams(n=1 << args.scale, seed=args.seed), device=True)
