@@ -85,7 +85,7 @@ def algorithmic_bytes(levels, n_dev: int, n_plus_dev: int) -> int:
     for i, r in enumerate(levels):
         reached += r.n_f
         n_next = levels[i + 1].n_f if i + 1 < len(levels) else 0
-        if r.direction == "top_down":
+        if (getattr(r, "executed_direction", None) or r.direction) == "top_down":  # the work actually done
             total += r.n_f * 20 + 4 * r.scanned_edges + n_next * 8
         else:
             U = max(n_plus_dev - reached, 0)

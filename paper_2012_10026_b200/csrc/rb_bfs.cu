@@ -73,6 +73,7 @@ constexpr int64_t kDenseFrontier = 8192;         // top-down: word-granular deal
 constexpr int kBU = 8;                           // bottom-up: max words per warp step (template KB <= kBU)
 constexpr int64_t kSmallGraph = 1ll << 23;       // n_dev up to this: 4-word bottom-up steps (shorter chains)
 constexpr int kList = 256;                       // top-down: rows per warp list round
+constexpr int64_t kExecAlpha = 14;               // execution: early bottom-up only if m_f > m_u / 14 (Beamer)
 constexpr int kK2 = 258;                         // bottom-up: per-lane checks before the warp takes over
 constexpr int kHeavyPerLane = 8;                 // warp-cooperative bottom-up: neighbours per lane per step
 constexpr uint64_t kDbgWarpBase = 65536;  // RB_DEBUG_TS buffer: per-block stamps, then per-warp stamps
@@ -159,6 +160,8 @@ struct KParams {
   int64_t max_levels;
   int64_t nf0, mf0, mu0;  // mf0 < 0: derive m_f / m_u from deg(src)
   int64_t from_fin;       // 1: traversal start; CTA 0 runs the first small levels alone (solo_levels)
+  int64_t exec_opt;       // pick the executed direction by cost (see kExecAlpha)
+  int64_t probe_mf;       // top-down: probe before claiming from this many frontier edges
   int64_t src;
   int64_t m_directed;
 };
@@ -917,7 +920,7 @@ __device__ __forceinline__ void solo_levels(const KParams& p, uint32_t* smem, So
       r.t_ns = (int64_t)(t_now - t_prev);
       r.n_next = n_next;
       r.t_queue_ns = 0;
-      r.reserved = 0;
+      r.reserved = dir;  // executed direction (solo levels: top-down)
       p.rec[done] = r;
       t_prev = t_now;
     }
@@ -1025,8 +1028,15 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
       reinterpret_cast<unsigned long long*>(p.slots + r1)[threadIdx.x] = 0ull;
     if (threadIdx.x == 0) s_bu_next[(L + 1) & 1] = 0u;  // the next level's counter (idle during this one)
 
+    // Execution direction.  The level keeps the reference policy's label
+    // (records, next decisions), but an early level labelled bottom-up (most
+    // edges still unvisited) whose frontier edges are few against the
+    // unvisited ones (m_f <= m_u / kExecAlpha) is executed top-down: most of
+    // its bottom-up scans would run to the end of their rows.  Same next
+    // frontier either way; any frontier neighbour is a valid parent.
+    const int xdir = (dir == 1 && p.exec_opt && 2 * mu > p.m_directed && mf * kExecAlpha <= mu) ? 0 : dir;
     Acc acc{0, 0, 0, 0u};
-    if (dir == 0) {
+    if (xdir == 0) {
       QEnt* hq = (L & 1) ? p.hq1 : p.hq0;
       TdCtx c;
       c.p = &p;
@@ -1034,7 +1044,10 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
       c.fcur = fcur;
       c.fnext = fnext;
       c.nznext = nz_of(p, r1);
-      c.probe = 2 * mu < p.m_directed;  // fewer than half the edge ends unvisited
+      // probe the visited word before the atomic when most targets are
+      // already taken: late levels, or big levels whose frontier rows share
+      // many neighbours (RB_PROBE_MF: from this many frontier edges)
+      c.probe = 2 * mu < p.m_directed || mf >= p.probe_mf;
       // phase A: frontier rows from the bitmap; hub rows become slices in hq
       if (nf >= kDenseFrontier)
         td_rows_words(c, hq, &in->hq_count, acc, s_bu_pair[threadIdx.x >> 5], &s_bu_next[L & 1]);
@@ -1085,7 +1098,7 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
       r.t_ns = (int64_t)(t_now - t_prev);
       r.n_next = n_next;
       r.t_queue_ns = (int64_t)t_queue;
-      r.reserved = 0;
+      r.reserved = xdir;  // executed direction
       p.rec[done] = r;
       t_queue = 0;
       t_prev = t_now;
@@ -1212,7 +1225,9 @@ struct rb_bfs {
   int64_t levels_per_launch;  // kRecCap; RB_LEVELS_PER_LAUNCH=1 gives one launch per level (profiling)
   cudaEvent_t ev_start, ev_end;  // bracket all launches of one traversal
   bool launched;
-  bool solo;  // run the first small levels in one CTA (bfs_solo); RB_SOLO=0 disables
+  bool solo;      // run the first small levels in one CTA (solo_levels); RB_SOLO=0 disables
+  bool exec_opt;  // executed direction by cost; RB_EXEC_OPT=0 disables
+  int64_t probe_mf;
   void* stream;
 };
 
@@ -1260,6 +1275,10 @@ extern "C" int rb_bfs_create_part(const int64_t* d_row_starts, const int32_t* d_
   h->levels_per_launch = kRecCap;
   h->solo = true;
   if (const char* env = getenv("RB_SOLO")) h->solo = atoi(env) != 0;
+  h->exec_opt = true;
+  if (const char* env = getenv("RB_EXEC_OPT")) h->exec_opt = atoi(env) != 0;
+  h->probe_mf = 1ll << 16;
+  if (const char* env = getenv("RB_PROBE_MF")) h->probe_mf = atoll(env);
   cudaEventCreate(&h->ev_start);
   cudaEventCreate(&h->ev_end);
   if (const char* env = getenv("RB_DEBUG")) h->kp.debug = atoi(env);
@@ -1436,6 +1455,8 @@ static int launch(rb_bfs* h, cudaStream_t s, int64_t level0, int64_t dir0, int64
   kp.src = h->source;
   kp.m_directed = h->prm.m_directed;
   kp.from_fin = from_fin;
+  kp.exec_opt = h->exec_opt ? 1 : 0;
+  kp.probe_mf = h->probe_mf;
   void* args[] = {&kp};
   cudaError_t e;
   e = cudaLaunchCooperativeKernel(bfs_kernel(h), dim3(h->blocks), dim3(kThreads), args, 0, s);

@@ -140,6 +140,9 @@ class LevelRecord:
     live_vertices: int | None = None
     claimed: int | None = None
     queue_time: float = 0.0  # device seconds of this level spent rebuilding top-down queues
+    # how the device ran the level: the policy's label is `direction`; a level
+    # labelled bottom-up with few frontier edges may run top-down
+    executed_direction: str | None = None
 
 
 @dataclass
@@ -311,6 +314,7 @@ def _records_to_levels(recs) -> list:
                 level=int(r.level), direction=TOP_DOWN if r.direction == 0 else BOTTOM_UP, n_f=int(r.n_f),
                 m_f=int(r.m_f), m_u=int(r.m_u), scanned_edges=int(r.scanned_edges), wall_time=r.t_ns * 1e-9,
                 per_thread_edges=np.array([int(r.scanned_edges)], dtype=np.int64), queue_time=r.t_queue_ns * 1e-9,
+                executed_direction=TOP_DOWN if r.reserved == 0 else BOTTOM_UP,
             )
         )
     return out

@@ -45,8 +45,9 @@ with rb.BfsEngine(g2, rb.BfsParams(mode=a.mode)) as eng:
             flush.zero_()
         el_s, levels = eng.run_device(int(s))
         print(f"root {s}: {el_s*1e6:.1f} us, levels {len(levels)}  " + " ".join(
-            f"{r.direction[0].upper()}{r.wall_time*1e6:.0f}" for r in levels))
+            f"{r.direction[0].upper()}{'' if (r.executed_direction or r.direction) == r.direction else '>' + r.executed_direction[0].upper()}{r.wall_time*1e6:.0f}" for r in levels))
         if a.brief:
             continue
         for r in levels:
-            print(f"   L{r.level} {r.direction[:1].upper()} n_f={r.n_f:9d} m_f={r.m_f:11d} scanned={r.scanned_edges:11d} t={r.wall_time*1e6:8.1f}us (queue {r.queue_time*1e6:6.1f})")
+            x = "" if (r.executed_direction or r.direction) == r.direction else ">" + r.executed_direction[0].upper()
+            print(f"   L{r.level} {r.direction[:1].upper()}{x} n_f={r.n_f:9d} m_f={r.m_f:11d} scanned={r.scanned_edges:11d} t={r.wall_time*1e6:8.1f}us (queue {r.queue_time*1e6:6.1f})")
