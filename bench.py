@@ -75,22 +75,54 @@ def hmean(x):
 # byte model, per root, from the level records
 
 
-def algorithmic_bytes(levels, n_dev: int, n_plus_dev: int) -> int:
+def level_bytes(levels, n_dev: int, n_plus_dev: int):
     """SURVEY.md 8(d) byte model without its per-vertex level term (the engine,
-    like the reference, keeps no level array unless asked to):
+    like the reference, keeps no level array unless asked to), per level:
     TD level: |F|*(4 queue + 16 offsets) + 4*E_TD + n_next*(4 parent + 4 queue)
-    BU level: 3*(n_dev/8) + 8*U + 4*C + n_next*(4 parent)."""
-    total = 0
+    BU level: 3*(n_dev/8) + 8*U + 4*C + n_next*(4 parent).
+    Returns [(executed direction, bytes, device seconds)] per level."""
+    out = []
     reached = 0
     for i, r in enumerate(levels):
         reached += r.n_f
         n_next = levels[i + 1].n_f if i + 1 < len(levels) else 0
-        if (getattr(r, "executed_direction", None) or r.direction) == "top_down":  # the work actually done
-            total += r.n_f * 20 + 4 * r.scanned_edges + n_next * 8
+        d = getattr(r, "executed_direction", None) or r.direction  # the work actually done
+        if d == "top_down":
+            b = r.n_f * 20 + 4 * r.scanned_edges + n_next * 8
         else:
             U = max(n_plus_dev - reached, 0)
-            total += 3 * (n_dev // 8) + 8 * U + 4 * r.scanned_edges + n_next * 4
-    return int(total)
+            b = 3 * (n_dev // 8) + 8 * U + 4 * r.scanned_edges + n_next * 4
+        out.append((d, int(b), float(r.wall_time)))
+    return out
+
+
+def algorithmic_bytes(levels, n_dev: int, n_plus_dev: int) -> int:
+    return int(sum(b for _, b, _ in level_bytes(levels, n_dev, n_plus_dev)))
+
+
+def by_direction(per_root, peak):
+    """Roofline per step kind (top-down / bottom-up levels of all timed roots):
+    sum of algorithmic bytes / sum of level device time (%globaltimer spans,
+    the grid barrier closing each level included)."""
+    out = {}
+    for d, key in (("top_down", "top_down"), ("bottom_up", "bottom_up")):
+        B = sum(b for lv in per_root for (x, b, _) in lv if x == d)
+        T = sum(t for lv in per_root for (x, _, t) in lv if x == d)
+        n = sum(1 for lv in per_root for (x, _, _) in lv if x == d)
+        out[key] = {"levels": n, "bytes": B, "seconds": T,
+                    "achieved": (B / T / 1e9) if T > 0 else None,
+                    "frac": (B / T / 1e9 / peak) if T > 0 else None}
+    # the dominant level of each kind (largest byte volume): the kernel phases
+    # the north star's 50% target is about
+    for d in ("top_down", "bottom_up"):
+        big = [max((y for y in lv if y[0] == d), key=lambda y: y[1], default=None) for lv in per_root]
+        big = [y for y in big if y is not None]
+        if big:
+            B = sum(y[1] for y in big)
+            T = sum(y[2] for y in big)
+            out[d]["largest_level"] = {"bytes_mean": B / len(big), "achieved": B / T / 1e9,
+                                       "frac": B / T / 1e9 / peak}
+    return out
 
 
 class ClockSampler:
@@ -334,7 +366,7 @@ def run_ours(args):
         eng.run_device(int(roots[my[i % len(my)]]))
     torch.cuda.synchronize()
 
-    times, teps, teps_dedup, bytes_alg, lvl_counts = [], [], [], [], []
+    times, teps, teps_dedup, bytes_alg, lvl_counts, per_root = [], [], [], [], [], []
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
@@ -348,7 +380,8 @@ def run_ours(args):
             times.append(el_s)
             teps.append(raw[j] / el_s)
             teps_dedup.append((sum(r.m_f for r in levels) // 2) / el_s)
-            bytes_alg.append(algorithmic_bytes(levels, n_dev, n_plus_dev))
+            per_root.append(level_bytes(levels, n_dev, n_plus_dev))
+            bytes_alg.append(sum(b for _, b, _ in per_root[-1]))
             lvl_counts.append(len(levels))
         ev_b.record()
         torch.cuda.synchronize()
@@ -417,7 +450,8 @@ def run_ours(args):
                      "peak_kind": peak_kind, "kernel": "bfs_persistent",
                      "bytes_per_launch": float(np.mean(bytes_alg)),
                      "launch_ms": 1e3 * float(np.mean(times)),
-                     "traffic": None if traffic is None else traffic.get("bytes_per_launch")},
+                     "traffic": None if traffic is None else traffic.get("bytes_per_launch"),
+                     "by_direction": by_direction(per_root, peak)},
         "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": 8, "d2h_bytes_per_step": int(d2h),
                 "api": "BfsEngine.run(source) -> BfsResult with host predecessor"},
         "validation": {"roots": n_val, "passed": n_ok,

@@ -59,6 +59,22 @@ namespace {
 #define RB_THREADS 1024
 #endif
 constexpr int kThreads = RB_THREADS;
+// Level bodies are separate (non-inlined) functions: each gets its own
+// register allocation under the 64-register cap instead of sharing one with
+// the whole persistent loop (fewer spills in the bottom-up hot loop).
+#ifndef RB_NOINLINE
+#define RB_NOINLINE 0  // measured: separate functions spill across the call ABI (s26 +35%)
+#endif
+#if RB_NOINLINE
+#define RB_LEVEL_FN __device__ __noinline__
+#else
+#define RB_LEVEL_FN __device__
+#endif
+// hot[] layout: 1 = {first neighbour in scan order, degree} (8 B: one load
+// and one probe per unvisited vertex); 0 = {first, second neighbour} + deg[].
+#ifndef RB_HOT1
+#define RB_HOT1 0  // measured: +1 probe-free byte saving loses on the first bottom-up level
+#endif
 #ifndef RB_MINB
 #define RB_MINB 1
 #endif
@@ -74,6 +90,14 @@ constexpr int kBU = 8;                           // bottom-up: max words per war
 constexpr int64_t kSmallGraph = 1ll << 23;       // n_dev up to this: 4-word bottom-up steps (shorter chains)
 constexpr int kList = 256;                       // top-down: rows per warp list round
 constexpr int64_t kExecAlpha = 14;               // execution: early bottom-up only if m_f > m_u / 14 (Beamer)
+// late-level execution cost model (picoseconds; measured level times at s22 / s26)
+constexpr int64_t kTdFixPs = 7000000;   // a top-down level: summary walk + barriers
+constexpr int64_t kTdRowPs = 18;        // per frontier row (record load, list)
+constexpr int64_t kTdEdgePs = 7;        // per frontier edge (probe / claim)
+constexpr int64_t kBuFixPs = 3000000;   // a bottom-up level: zeroing + barrier
+constexpr int64_t kBuStepPs = 650000;   // per warp step of the bitmap pass (dependent chain)
+constexpr int64_t kBuVertPs = 5;        // per unvisited vertex
+constexpr int64_t kBuCheckPs = 1;       // per neighbour check (bounded by 8 per unvisited vertex)
 constexpr int kK2 = 258;                         // bottom-up: per-lane checks before the warp takes over
 constexpr int kHeavyPerLane = 8;                 // warp-cooperative bottom-up: neighbours per lane per step
 constexpr uint64_t kDbgWarpBase = 65536;  // RB_DEBUG_TS buffer: per-block stamps, then per-warp stamps
@@ -112,6 +136,8 @@ struct Final {  // state after a launch (continuation for very deep graphs)
   long long need_compact;
   long long nf, mf, mu;
   long long pad;
+  long long reached;  // vertices discovered so far (frontier included)
+  long long pad2;
 };
 
 struct KParams {
@@ -162,8 +188,11 @@ struct KParams {
   int64_t from_fin;       // 1: traversal start; CTA 0 runs the first small levels alone (solo_levels)
   int64_t exec_opt;       // pick the executed direction by cost (see kExecAlpha)
   int64_t probe_mf;       // top-down: probe before claiming from this many frontier edges
+  int64_t defer_mf;       // top-down: fire-and-forget claims + count_next from this many frontier edges
   int64_t src;
   int64_t m_directed;
+  int64_t n_active;  // non-isolated vertices in [0, n_dev) (executed-direction cost model)
+  int64_t reached0;  // vertices discovered before this launch
 };
 
 __device__ __forceinline__ uint32_t* fb_of(const KParams& p, int r) {  // r = level % 3
@@ -206,6 +235,7 @@ struct TdCtx {
   uint32_t* fnext;
   uint8_t* nznext;
   bool probe;  // probe visited bits before the atomic (most targets visited)
+  bool defer;  // fire-and-forget claims; the next frontier is counted after the level (count_next)
 };
 
 __device__ __forceinline__ QEnt ld_qent(const QEnt* q) {
@@ -239,6 +269,37 @@ __device__ __forceinline__ void td_claim(const TdCtx& c, const int32_t (&v)[KU],
   int32_t wl[KU];
 #pragma unroll
   for (int k = 0; k < KU; ++k) wl[k] = w[k] - (int32_t)p.v_lo;
+#ifdef RB_TD_EXPERIMENT  // timing experiments only (wrong results): 1 = columns only, 2 = + probes
+  if (c.defer) {
+    uint32_t x = 0;
+#pragma unroll
+    for (int k = 0; k < KU; ++k) x += (RB_TD_EXPERIMENT >= 2 && act[k]) ? ld_bits(p.vis + (wl[k] >> 5)) : (uint32_t)wl[k];
+    if (x == 0x12345678u) p.parent[0] = (int32_t)x;
+    return;
+  }
+#endif
+  if (c.defer) {
+    // Big levels: no atomic return trip and no per-winner degree load.  Every
+    // frontier vertex adjacent to an unvisited w is a valid parent of w, so
+    // concurrent writers of parent[w] may race -- the last store stands.  Only
+    // the visited bit is set (fire-and-forget red; it also stops later probes
+    // of this level): the next frontier is vis minus the copy of vis taken at
+    // the level start (held in fnext), and its summary and exact counters
+    // (n_next, deg_next, max degree) come from one pass over it (count_next).
+    uint32_t seen[KU];
+#pragma unroll
+    for (int k = 0; k < KU; ++k) seen[k] = act[k] ? ld_bits(p.vis + (wl[k] >> 5)) : 0u;
+#pragma unroll
+    for (int k = 0; k < KU; ++k) {
+      const uint32_t bit = 1u << (wl[k] & 31);
+      if (act[k] && !(seen[k] & bit)) {
+        p.parent[wl[k]] = v[k];
+        if (p.level) p.level[wl[k]] = (int32_t)(c.L + 1);
+        red_or(p.vis + (wl[k] >> 5), bit);
+      }
+    }
+    return;
+  }
   // claim = first to set the visited bit (vis holds every discovered vertex).
   // Late levels (most targets already visited) first probe with a plain,
   // L1-cacheable load -- bits only ever get set, so a stale probe can only
@@ -427,7 +488,7 @@ __device__ __forceinline__ void td_list(const TdCtx& c, const uint32_t* lst, uin
 // batch ahead, its words in flight).  The nonzero words of a batch are
 // compacted into the warp's shared-memory list, at most 256 rows per round
 // (popc + warp scan + a loop over each lane's set bits).
-__device__ void td_rows_words(const TdCtx& c, QEnt* hq, unsigned long long* hq_count, Acc& acc, uint32_t* lst,
+RB_LEVEL_FN void td_rows_words(const TdCtx& c, QEnt* hq, unsigned long long* hq_count, Acc& acc, uint32_t* lst,
                               uint32_t* s_next) {
   const KParams& p = *c.p;
   const uint32_t lane = rb::lane_id();
@@ -470,7 +531,7 @@ __device__ void td_rows_words(const TdCtx& c, QEnt* hq, unsigned long long* hq_c
 // the nonzero summary (each bit covers one bitmap word, a byte one 256-vertex
 // item) strided over the whole range, so one load skips 32 empty items; a
 // nonzero item is compacted into the warp's list (lane l owns byte l).
-__device__ void td_rows_items(const TdCtx& c, const uint8_t* nzcur, QEnt* hq, unsigned long long* hq_count,
+RB_LEVEL_FN void td_rows_items(const TdCtx& c, const uint8_t* nzcur, QEnt* hq, unsigned long long* hq_count,
                               Acc& acc, uint32_t* lst) {
   const KParams& p = *c.p;
   const uint32_t lane = rb::lane_id();
@@ -507,27 +568,90 @@ __device__ void td_rows_items(const TdCtx& c, const uint8_t* nzcur, QEnt* hq, un
   }
 }
 
+// End of a deferred top-down level: fnext (holding vis as it was at the
+// level start) becomes the next frontier vis & ~fnext, with its nonzero
+// summary; counters n_next = popcount, deg_next = sum of the degrees of the
+// new bits (one coalesced 128-B load of deg[] per nonzero word, 4 words in
+// flight), max degree.  Streaming passes instead of per-claim random traffic.
+__device__ void count_next(const KParams& p, uint32_t* fnext, uint8_t* nznext, Acc& acc) {
+  const uint32_t lane = rb::lane_id();
+  const uint64_t nw = (uint64_t)p.n_words;
+  const uint64_t stride = (uint64_t)gridDim.x * kWarps * 32;
+  for (uint64_t w0 = warp_slot() * 32; w0 < nw; w0 += stride) {
+    const uint32_t x = __ldcg(p.vis + w0 + lane) & ~__ldcg(fnext + w0 + lane);
+    fnext[w0 + lane] = x;
+    nznext[w0 + lane] = x != 0u ? 1u : 0u;
+    acc.n += __popc(x);
+    uint32_t m = __ballot_sync(RB_FULL, x != 0u);
+    while (m) {
+      uint32_t d[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        d[q] = 0u;
+        if (m) {
+          const uint32_t j = __ffs(m) - 1;
+          m &= m - 1;
+          const uint32_t xj = __shfl_sync(RB_FULL, x, j);  // m is warp-uniform
+          if ((xj >> lane) & 1u) d[q] = (uint32_t)rb::ldg_i32(p.deg + (int64_t)(w0 + j) * 32 + lane);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        acc.deg += d[q];
+        acc.maxdeg = max(acc.maxdeg, d[q]);
+      }
+    }
+  }
+}
+
 // Top-down phase B: hub slices, one warp item each (8 edges per lane).
-__device__ void td_hubs(const TdCtx& c, const QEnt* hq, uint64_t nh, Acc& acc) {
+RB_LEVEL_FN void td_hubs(const TdCtx& c, const QEnt* hq, uint64_t nh, Acc& acc) {
+  // Software-pipelined over the warp's slices: while slice i is probed and
+  // claimed, the columns of slice i+1 and the entry of slice i+2 are in
+  // flight (a slice is otherwise a chain entry -> columns -> probes).
   const KParams& p = *c.p;
   const uint32_t lane = rb::lane_id();
   const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
-  for (uint64_t item = warp_slot(); item < nh; item += nwarps) {
-    const QEnt ent = ld_qent(hq + item);
-    const int32_t v = ent.v;
-    const int64_t a = ent.s;
-    const int64_t b = a + ent.d;
-    if (lane == 0) acc.scan += (unsigned long long)(b - a);
-    int32_t vv[kChunkPerLane], w[kChunkPerLane];
+  uint64_t item = warp_slot();
+  if (item >= nh) return;
+  auto entry = [&](uint64_t i) -> QEnt {
+    if (i < nh) return ld_qent(hq + i);
+    QEnt z;
+    z.s = 0;
+    z.v = 0;
+    z.d = 0;
+    return z;
+  };
+  auto columns = [&](const QEnt& e, int32_t (&w)[kChunkPerLane]) {
+#pragma unroll
+    for (int k = 0; k < kChunkPerLane; ++k) {
+      const int32_t j = (int32_t)lane + 32 * k;
+      w[k] = j < e.d ? rb::ldg_i32(p.td_col + e.s + j) : -1;
+    }
+  };
+  QEnt e = entry(item);
+  QEnt e2 = entry(item + nwarps);
+  int32_t w[kChunkPerLane];
+  columns(e, w);
+  while (true) {
+    const QEnt e3 = entry(item + 2 * nwarps);
+    int32_t w2[kChunkPerLane];
+    columns(e2, w2);
+    if (lane == 0) acc.scan += (unsigned long long)e.d;
+    int32_t vv[kChunkPerLane];
     bool act[kChunkPerLane];
 #pragma unroll
     for (int k = 0; k < kChunkPerLane; ++k) {
-      const int64_t j = a + lane + 32 * k;
-      act[k] = j < b;
-      vv[k] = v;
-      w[k] = act[k] ? rb::ldg_i32(p.td_col + j) : 0;
+      vv[k] = e.v;
+      act[k] = w[k] >= 0;
     }
     td_claim<kChunkPerLane>(c, vv, w, act, acc);
+    item += nwarps;
+    if (item >= nh) break;
+    e = e2;
+    e2 = e3;
+#pragma unroll
+    for (int k = 0; k < kChunkPerLane; ++k) w[k] = w2[k];
   }
 }
 
@@ -578,7 +702,7 @@ __device__ __forceinline__ int32_t bu_heavy(const KParams& p, const uint32_t* fc
 }
 
 template <bool kRev, int KB>
-__device__ void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uint32_t* fnext, uint8_t* nznext,
+RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uint32_t* fnext, uint8_t* nznext,
                          Acc& acc, uint32_t* s_found, uint32_t* s_pair, uint32_t* s_next) {
   const uint32_t lane = rb::lane_id();
   const uint64_t nw = (uint64_t)p.n_words;
@@ -608,7 +732,35 @@ __device__ void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uint
     if (!__any_sync(RB_FULL, actm != 0)) continue;
     const int64_t vbase = (int64_t)w0 * 32 + lane;
     const int2* const hot = p.hot + vbase;
+#if !RB_HOT1
     const int32_t* const deg = p.deg + vbase;
+#endif
+#if RB_HOT1
+    // round 1: the scan-first neighbour and the degree from the compact
+    // `hot` side array (8 B per vertex, coalesced) -- all KB loads in flight
+    int2 hv[KB];
+#pragma unroll
+    for (int k = 0; k < KB; ++k) hv[k] = ((actm >> k) & 1u) ? __ldg(hot + 32 * k) : make_int2(-1, 0);
+    uint32_t hb0[KB];
+#pragma unroll
+    for (int k = 0; k < KB; ++k) hb0[k] = hv[k].x >= 0 ? ld_bits(fcur + (hv[k].x >> 5)) : 0u;
+    uint32_t dg[KB];
+    uint32_t foundm = 0, needm = 0, checks = 0, dsum = 0, dmax = 0;
+    int32_t* const par_out = p.parent + vbase;
+#pragma unroll
+    for (int k = 0; k < KB; ++k) {
+      const bool act = (actm >> k) & 1u;
+      dg[k] = (uint32_t)hv[k].y;
+      const bool found = act && hv[k].x >= 0 && ((hb0[k] >> (hv[k].x & 31)) & 1u);
+      checks += (act && dg[k]) ? 1u : 0u;
+      if (found) par_out[32 * k] = hv[k].x;
+      foundm |= (uint32_t)found << k;
+      needm |= (uint32_t)(act && !found && dg[k] > 1u) << k;
+      dsum += found ? dg[k] : 0u;
+      dmax = max(dmax, found ? dg[k] : 0u);
+    }
+    constexpr int kFirst = 1;  // checks done by round 1 on a continuing row
+#else
     // round 1: the two scan-first neighbours from the compact `hot` side
     // array (8 B per vertex, coalesced) -- all KB loads in flight
     int2 hv[KB];
@@ -644,6 +796,8 @@ __device__ void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uint
       dsum += found ? dg[k] : 0u;
       dmax = max(dmax, found ? dg[k] : 0u);
     }
+    constexpr int kFirst = 2;
+#endif
     if (foundm && level_out) {
 #pragma unroll
       for (int k = 0; k < KB; ++k)
@@ -686,7 +840,7 @@ __device__ void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uint
           const int64_t e0 = s0 + d;
           const int64_t lim = d < (uint32_t)kK2 ? d : kK2;
           // contiguous 8-neighbour chunks of the row: one sector per lane per step
-          for (int64_t t0 = 2; par < 0 && t0 < lim; t0 += 8) {
+          for (int64_t t0 = kFirst; par < 0 && t0 < lim; t0 += 8) {
             int32_t uu[8];
             uint32_t bb[8];
 #pragma unroll
@@ -815,7 +969,7 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* warp_t
 // level that is not run solo (or the end of the traversal).
 __device__ __forceinline__ void solo_levels(const KParams& p, uint32_t* smem, SoloShared* sh, uint32_t* warp_tot, int64_t& L,
                             int& dir, int64_t& nf, int64_t& mf, int64_t& mu, int64_t& done, bool& hubs,
-                            uint64_t& t_prev) {
+                            uint64_t& t_prev, int64_t& reached) {
   const uint32_t tid = threadIdx.x;
   uint32_t* qp = smem;                 // frontier of level L-1
   uint32_t* qc = smem + kSoloCap;      // frontier of level L
@@ -927,6 +1081,7 @@ __device__ __forceinline__ void solo_levels(const KParams& p, uint32_t* smem, So
     mu -= deg_next;
     mf = deg_next;
     nf = n_next;
+    reached += n_next;
     int ndir = 0;
     if (p.hybrid) {
       if (dir == 0)
@@ -972,6 +1127,7 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
     mu = p.m_directed - mf;
   }
   int64_t done = 0;
+  int64_t reached = p.reached0;
   uint32_t epoch = 0;
   bool solo_hubs = false;
   if (p.from_fin && mf <= kSoloMf) {
@@ -980,8 +1136,9 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
     if (blockIdx.x == 0) {
       uint64_t t0 = globaltimer();
       bool h = false;
-      solo_levels(p, &s_bu_pair[0][0], &s_solo, s_wtot, L, dir, nf, mf, mu, done, h, t0);
+      solo_levels(p, &s_bu_pair[0][0], &s_solo, s_wtot, L, dir, nf, mf, mu, done, h, t0, reached);
       if (threadIdx.x == 0) {
+        p.fin->reached = reached;
         p.fin->levels_done = done;
         p.fin->L = L;
         p.fin->dir = dir;
@@ -999,6 +1156,7 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
     mf = (int64_t)rb::ld_relaxed_u64((const unsigned long long*)&p.fin->mf);
     mu = (int64_t)rb::ld_relaxed_u64((const unsigned long long*)&p.fin->mu);
     solo_hubs = rb::ld_relaxed_u64((const unsigned long long*)&p.fin->pad) != 0;
+    reached = (int64_t)rb::ld_relaxed_u64((const unsigned long long*)&p.fin->reached);
     need_compact = dir == 0;
   }
   int r0 = (int)(L % 3);
@@ -1029,12 +1187,29 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
     if (threadIdx.x == 0) s_bu_next[(L + 1) & 1] = 0u;  // the next level's counter (idle during this one)
 
     // Execution direction.  The level keeps the reference policy's label
-    // (records, next decisions), but an early level labelled bottom-up (most
-    // edges still unvisited) whose frontier edges are few against the
-    // unvisited ones (m_f <= m_u / kExecAlpha) is executed top-down: most of
-    // its bottom-up scans would run to the end of their rows.  Same next
+    // (records, next decisions); the work is done the cheaper way.  Same next
     // frontier either way; any frontier neighbour is a valid parent.
-    const int xdir = (dir == 1 && p.exec_opt && 2 * mu > p.m_directed && mf * kExecAlpha <= mu) ? 0 : dir;
+    //  * early (most edges unvisited), labelled bottom-up: executed top-down
+    //    when the frontier edges are few against the unvisited ones (m_f <=
+    //    m_u / kExecAlpha) -- most bottom-up scans would run to the row end;
+    //  * late (most edges visited), either label: a latency cost model in
+    //    picoseconds -- top-down pays per frontier row and edge, bottom-up
+    //    pays a bitmap pass (step chain per warp) plus per unvisited vertex.
+    //    After the big bottom-up levels the frontier is millions of leaves
+    //    but only thousands of vertices are still unvisited: bottom-up wins
+    //    5x; the tail frontiers of a few thousand rows go top-down.
+    int xdir = dir;
+    if (p.exec_opt) {
+      if (2 * mu > p.m_directed) {
+        if (dir == 1 && mf * kExecAlpha <= mu) xdir = 0;
+      } else {
+        const int64_t U = p.n_active > reached ? p.n_active - reached : 0;
+        const int64_t t_td = kTdFixPs + nf * kTdRowPs + mf * kTdEdgePs;
+        const int64_t t_bu = kBuFixPs + (p.n_words / KB) * kBuStepPs / ((int64_t)nblocks * kWarps) + U * kBuVertPs +
+                             min(mu, 8 * U) * kBuCheckPs;
+        xdir = t_td <= t_bu ? 0 : 1;
+      }
+    }
     Acc acc{0, 0, 0, 0u};
     if (xdir == 0) {
       QEnt* hq = (L & 1) ? p.hq1 : p.hq0;
@@ -1048,6 +1223,12 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
       // already taken: late levels, or big levels whose frontier rows share
       // many neighbours (RB_PROBE_MF: from this many frontier edges)
       c.probe = 2 * mu < p.m_directed || mf >= p.probe_mf;
+      c.defer = mf >= p.defer_mf;
+      if (c.defer) {  // snapshot of vis at the level start (see count_next)
+        for (uint64_t i = gtid; i < (uint64_t)p.n_words / 4; i += gthreads)
+          reinterpret_cast<uint4*>(fnext)[i] = __ldcg(reinterpret_cast<const uint4*>(p.vis) + i);
+        rb::grid_barrier(p.bar, nblocks, epoch);
+      }
       // phase A: frontier rows from the bitmap; hub rows become slices in hq
       if (nf >= kDenseFrontier)
         td_rows_words(c, hq, &in->hq_count, acc, s_bu_pair[threadIdx.x >> 5], &s_bu_next[L & 1]);
@@ -1061,6 +1242,10 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
         }
         if (blockIdx.x == 0 && threadIdx.x == 32) t_queue = globaltimer() - t_prev;
         td_hubs(c, hq, s_ctr[0], acc);
+      }
+      if (c.defer) {
+        rb::grid_barrier(p.bar, nblocks, epoch);  // every claim of the level has landed
+        count_next(p, fnext, nz_of(p, r1), acc);
       }
     } else {
       const uint32_t wib = threadIdx.x >> 5;
@@ -1107,6 +1292,7 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
     mu -= deg_next;
     mf = deg_next;
     nf = n_next;
+    reached += n_next;
     int ndir = 0;
     if (p.hybrid) {
       if (dir == 0)
@@ -1128,6 +1314,7 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
     p.fin->nf = nf;
     p.fin->mf = mf;
     p.fin->mu = mu;
+    p.fin->reached = reached;
   }
 }
 
@@ -1155,16 +1342,30 @@ __global__ void make_vinfo(const int64_t* rs, const int32_t* col, int64_t n, VIn
   }
 }
 
-// hot[v] = the first two neighbours of v in bottom-up scan order (-1 if absent)
+// hot[v] (RB_HOT1): {first neighbour of v in bottom-up scan order (-1 if
+// none), degree}; else the first two neighbours (-1 if absent)
 __global__ void make_hot(const int64_t* rs, const int32_t* col, int64_t n, int reverse, int2* hot) {
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s = rs[v], e = rs[v + 1];
     const int64_t d = e - s;
     int2 h = make_int2(-1, -1);
     if (d > 0) h.x = reverse ? col[e - 1] : col[s];
+#if RB_HOT1
+    h.y = (int32_t)d;
+#else
     if (d > 1) h.y = reverse ? col[e - 2] : col[s + 1];
+#endif
     hot[v] = h;
   }
+}
+
+// *out += number of zero bits of words[0, n) (unvisited-at-start vertices)
+__global__ void count_zero_bits(const uint32_t* words, int64_t n, unsigned long long* out) {
+  unsigned long long c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    c += (unsigned long long)__popc(~words[i]);
+  c = rb::warp_sum_u64(c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
 }
 
 // nz[i] = words[i] != 0
@@ -1228,6 +1429,7 @@ struct rb_bfs {
   bool solo;      // run the first small levels in one CTA (solo_levels); RB_SOLO=0 disables
   bool exec_opt;  // executed direction by cost; RB_EXEC_OPT=0 disables
   int64_t probe_mf;
+  int64_t defer_mf;
   void* stream;
 };
 
@@ -1279,6 +1481,10 @@ extern "C" int rb_bfs_create_part(const int64_t* d_row_starts, const int32_t* d_
   if (const char* env = getenv("RB_EXEC_OPT")) h->exec_opt = atoi(env) != 0;
   h->probe_mf = 1ll << 16;
   if (const char* env = getenv("RB_PROBE_MF")) h->probe_mf = atoll(env);
+  h->defer_mf = 1ll << 20;
+  if (const char* env = getenv("RB_DEFER_MF")) h->defer_mf = atoll(env);
+  h->kp.probe_mf = h->probe_mf;  // also seen by rb_bfs_dist_level (which copies kp)
+  h->kp.defer_mf = h->defer_mf;
   cudaEventCreate(&h->ev_start);
   cudaEventCreate(&h->ev_end);
   if (const char* env = getenv("RB_DEBUG")) h->kp.debug = atoi(env);
@@ -1364,6 +1570,12 @@ extern "C" int rb_bfs_create_part(const int64_t* d_row_starts, const int32_t* d_
     return RB_ERR_CUDA;
   }
   if (d_isolated_words) words_or<<<256, 256>>>(h->vis_template, d_isolated_words, (n_dev + 31) / 32);
+  // non-isolated vertices of [0, n_dev): zero bits of the template (slot 0 is scratch here)
+  cudaMemset(k.slots, 0, sizeof(Slot));
+  count_zero_bits<<<256, 256>>>(h->vis_template, h->n_words, &k.slots->n_next);
+  unsigned long long n_active = 0;
+  cudaMemcpy(&n_active, &k.slots->n_next, 8, cudaMemcpyDeviceToHost);
+  k.n_active = (int64_t)n_active;
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     rb_set_error("rb_bfs_create: %s", cudaGetErrorString(e));
@@ -1443,7 +1655,8 @@ extern "C" int rb_bfs_reset(rb_bfs* h, int64_t source, void* stream) {
 }
 
 static int launch(rb_bfs* h, cudaStream_t s, int64_t level0, int64_t dir0, int64_t need_compact0, int64_t max_levels,
-                  int64_t nf0, int64_t mf0, int64_t mu0, int64_t from_fin = 0) {
+                  int64_t nf0, int64_t mf0, int64_t mu0, int64_t from_fin = 0, int64_t reached0 = 1,
+                  bool exec = true) {
   KParams kp = h->kp;
   kp.level0 = level0;
   kp.dir0 = dir0;
@@ -1455,8 +1668,10 @@ static int launch(rb_bfs* h, cudaStream_t s, int64_t level0, int64_t dir0, int64
   kp.src = h->source;
   kp.m_directed = h->prm.m_directed;
   kp.from_fin = from_fin;
-  kp.exec_opt = h->exec_opt ? 1 : 0;
+  kp.exec_opt = (exec && h->exec_opt) ? 1 : 0;
+  kp.reached0 = reached0;
   kp.probe_mf = h->probe_mf;
+  kp.defer_mf = h->defer_mf;
   void* args[] = {&kp};
   cudaError_t e;
   e = cudaLaunchCooperativeKernel(bfs_kernel(h), dim3(h->blocks), dim3(kThreads), args, 0, s);
@@ -1501,7 +1716,7 @@ extern "C" int rb_bfs_results(rb_bfs* h, int32_t* parent_out, int32_t* level_out
       }
       if (f.nf <= 0) break;
       RB_CUDA_TRY(cudaMemsetAsync(h->kp.bar, 0, 64, s));
-      int rc = launch(h, s, f.L, f.dir, f.need_compact, h->levels_per_launch, f.nf, f.mf, f.mu);
+      int rc = launch(h, s, f.L, f.dir, f.need_compact, h->levels_per_launch, f.nf, f.mf, f.mu, 0, f.reached);
       if (rc) return rc;
       RB_CUDA_TRY(cudaEventRecord(h->ev_end, s));
     }
@@ -1540,7 +1755,7 @@ extern "C" int rb_bfs_step(rb_bfs* h, int direction, const uint32_t* d_visited_w
   make_nz<<<256, 256, 0, s>>>(k.fb0, k.nz0, h->n_words);
   RB_CUDA_TRY(cudaMemcpyAsync(k.parent, d_parent_in, (size_t)h->n_dev * 4, cudaMemcpyDeviceToDevice, s));
   h->source = 0;
-  rc = launch(h, s, 0, direction, direction == 0 ? 1 : 0, 1, 1, 0, 0);
+  rc = launch(h, s, 0, direction, direction == 0 ? 1 : 0, 1, 1, 0, 0, 0, 1, false);  // the direction asked for
   if (rc) return rc;
   words_or3<<<256, 256, 0, s>>>(k.vis, k.fb0, k.fb1, d_visited_out, nw_in, h->pad_mask);
   RB_CUDA_TRY(cudaMemcpyAsync(d_next_out, k.fb1, (size_t)nw_in * 4, cudaMemcpyDeviceToDevice, s));

@@ -252,3 +252,27 @@ def test_random_states_all_step_kernels(cuda_ok):
                 assert np.array_equal(visited.words, ref_vis), fn.__name__
             states += 1
     assert states == 96
+
+
+@pytest.mark.parametrize("knobs", [{"RB_DEFER_MF": "0"}, {"RB_DEFER_MF": "0", "RB_SOLO": "0"},
+                                   {"RB_EXEC_OPT": "0"}, {"RB_DEFER_MF": "4096", "RB_PROBE_MF": "0"}])
+def test_engine_knobs_keep_parity(cuda_ok, ocache, monkeypatch, knobs):
+    """Execution knobs change HOW a level runs (deferred fire-and-forget claims
+    counted from the next-frontier bitmap, solo levels, the executed direction,
+    probing) -- never the levels, the records or tree validity."""
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    for scale, seed in ((14, 3), (16, 1)):
+        c = ocache.kron(scale, seed)
+        g2 = c["g2"]
+        labels = oracle.csr_components(g2)
+        with rb.BfsEngine(to_rb(g2), rb.BfsParams(mode="hybrid"), record_levels=True) as eng:
+            for s in oracle.sample_sources(g2.degrees, 6, scale):
+                s = int(s)
+                _, want, _, _ = oracle.seq_bfs(g2, s)
+                _, rec, _ = oracle.hybrid_bfs(g2, s)
+                res = eng.run(s)
+                lev = check_run(g2, labels, res, s, eng=eng)
+                assert np.array_equal(lev.astype(np.int32), want), (knobs, scale, s)
+                got = [(0 if r.direction == rb.TOP_DOWN else 1, r.n_f, r.m_f, r.m_u) for r in res.levels]
+                assert got == [tuple(int(x) for x in r[1:5]) for r in rec], (knobs, scale, s)

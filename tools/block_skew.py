@@ -22,7 +22,8 @@ g2 = rb.apply_permutation(g, perm)
 del g, el
 roots = rb.sample_sources(g2.device_arrays()[2].cpu().numpy(), 64, 1)
 with rb.BfsEngine(g2, rb.BfsParams()) as eng:
-    for r in roots[:2]:
+    idx = [int(x) for x in os.environ.get("RB_ROOT_INDEX", "0,1").split(",")]
+    for r in [roots[i] for i in idx]:
         eng.run_device(int(r))
         t, levels = eng.run_device(int(r))
         buf = np.zeros(65536 + 64 * 148 * 32, np.uint64)
@@ -31,7 +32,7 @@ with rb.BfsEngine(g2, rb.BfsParams()) as eng:
                                                       ctypes.byref(nb)))
         ts = buf[: 64 * 4 * nb.value].reshape(64, nb.value, 4).astype(np.int64)
         wt = buf[65536: 65536 + 64 * nb.value * 32].reshape(64, nb.value, 32).astype(np.int64)
-        print(f"root {int(r)}: {t * 1e6:.1f} us")
+        print(f"root {int(r)}: {t * 1e6:.1f} us  (level index L of the debug stamps counts grid levels only)")
         for L, rec in enumerate(levels):
             a, b, c = ts[L, :, 0], ts[L, :, 1], ts[L, :, 2]
             w = (b - a) / 1e3
