@@ -15,8 +15,8 @@
 //                fb[(L+2)%3] is zeroed during level L (it is fnext of L+1)
 //   nz[3][]      one byte per bitmap word: 1 = "word nonzero" (rotated with fb;
 //                plain byte stores, no atomics)
-//   hq[2]        hub slices {row offset, vertex, length}: one 16-B entry per
-//                256-edge slice of a frontier row longer than 32
+//   hq[2], hs[2] hub rows {row start, vertex, degree} and the first index of
+//                their 256-edge slices (phase B deals slices over all warps)
 //   vinfo[]      32-B row record {row start, degree, first two neighbours}
 //   hot[]        int2 per vertex: the first two neighbours in bottom-up order
 //   parent[]     int32; level[] only when the caller asks for it
@@ -83,16 +83,17 @@ constexpr uint32_t kLightDeg = 32;  // deg <= kLightDeg -> light queue
 constexpr uint32_t kTinyDeg = 2;    // deg <= kTinyDeg -> tiny queue (neighbours inline)
 constexpr int kChunkPerLane = 8;
 constexpr uint32_t kChunk = 32 * kChunkPerLane;  // edges per hub work item
+constexpr unsigned long long kSliceMask = (1ull << 40) - 1;  // hq_count: rows << 40 | slices
 constexpr int kTdUnroll = 4;                     // light batch: edges per lane per step
 constexpr int kUB = 4;                           // top-down: rows per lane per round
 constexpr int64_t kDenseFrontier = 8192;         // top-down: word-granular dealing from this frontier size
 constexpr int kBU = 8;                           // bottom-up: max words per warp step (template KB <= kBU)
 constexpr int64_t kSmallGraph = 1ll << 23;       // n_dev up to this: 4-word bottom-up steps (shorter chains)
 constexpr int kList = 256;                       // top-down: rows per warp list round
-constexpr int64_t kExecAlpha = 14;               // execution: early bottom-up only if m_f > m_u / 14 (Beamer)
+constexpr int64_t kExecAlpha = 11;               // execution: early bottom-up only if m_f > m_u / 11 (measured crossover, s22 and s26)
 // late-level execution cost model (picoseconds; measured level times at s22 / s26)
-constexpr int64_t kTdFixPs = 7000000;   // a top-down level: summary walk + barriers
-constexpr int64_t kTdRowPs = 18;        // per frontier row (record load, list)
+constexpr int64_t kTdFixPs = 8000000;   // a top-down level: summary walk + barriers
+constexpr int64_t kTdRowPs = 80;        // per frontier row (bitmap walk, record load, list)
 constexpr int64_t kTdEdgePs = 7;        // per frontier edge (probe / claim)
 constexpr int64_t kBuFixPs = 3000000;   // a bottom-up level: zeroing + barrier
 constexpr int64_t kBuStepPs = 650000;   // per warp step of the bitmap pass (dependent chain)
@@ -101,6 +102,7 @@ constexpr int64_t kBuCheckPs = 1;       // per neighbour check (bounded by 8 per
 constexpr int kK2 = 258;                         // bottom-up: per-lane checks before the warp takes over
 constexpr int kHeavyPerLane = 8;                 // warp-cooperative bottom-up: neighbours per lane per step
 constexpr uint64_t kDbgWarpBase = 65536;  // RB_DEBUG_TS buffer: per-block stamps, then per-warp stamps
+constexpr uint64_t kDbgPhase = 60000;     // RB_DEBUG_TS: CTA 0 phase stamps, 8 per level (top-down sub-phases)
 constexpr int64_t kRecCap = 4096;                // level records per launch
 
 // Queue entry: a light frontier row (d <= kLightDeg) or one hub slice
@@ -124,7 +126,7 @@ struct Slot {  // per-level counters, triple-buffered by level % 3
   unsigned long long n_next;
   unsigned long long deg_next;
   unsigned long long scanned;
-  unsigned long long hq_count;  // hub slices appended by phase A of the NEXT level
+  unsigned long long hq_count;  // hub rows << 40 | their 256-edge slices, appended by phase A of the NEXT level
   unsigned long long maxdeg;    // max degree of the next frontier (hub slices needed?)
   unsigned long long pad1, pad2, pad3;
 };
@@ -168,8 +170,10 @@ struct KParams {
   const uint32_t* fcur_ext;   // if set: the (all-gathered) global frontier bitmap of this level
   const uint8_t* nzcur_ext;  // and its nonzero summary (one byte per word)
   int64_t hubs0;              // -1: derive from deg(src); 0 / 1: forced (distributed levels)
-  QEnt* hq0;           // hub slices of the current top-down level (alternating)
+  QEnt* hq0;           // hub rows of the current top-down level (alternating)
   QEnt* hq1;
+  uint32_t* hs0;       // first slice index of each hub row (ascending)
+  uint32_t* hs1;
   int32_t* parent;
   int32_t* level;
   Slot* slots;
@@ -189,6 +193,8 @@ struct KParams {
   int64_t exec_opt;       // pick the executed direction by cost (see kExecAlpha)
   int64_t probe_mf;       // top-down: probe before claiming from this many frontier edges
   int64_t defer_mf;       // top-down: fire-and-forget claims + count_next from this many frontier edges
+  int64_t td_m;           // entries of td_col
+  int64_t exec_alpha;     // early levels labelled bottom-up run top-down if m_f * exec_alpha <= m_u
   int64_t src;
   int64_t m_directed;
   int64_t n_active;  // non-isolated vertices in [0, n_dev) (executed-direction cost model)
@@ -339,59 +345,61 @@ __device__ __forceinline__ void td_claim(const TdCtx& c, const int32_t (&v)[KU],
   }
 }
 
-// Warp-aggregated append of hub rows (deg > kLightDeg) as kChunk-edge slices:
-// one atomic per warp reserves the range, all 32 lanes write slices in
-// parallel (a lane holding a huge row does not serialize the warp).
+// Warp-aggregated append of hub rows (deg > kLightDeg): one entry per row
+// {row start, vertex, degree} plus its first slice index.  One 64-bit atomic
+// per warp reserves rows and slices together (rows << 40 | slices), so the
+// slice starts ascend with the row index and phase B maps a slice to its row
+// by search; a row of a million edges costs one entry, not 4000.
 template <int KU>
-__device__ __forceinline__ void warp_push_slices(QEnt* hq, unsigned long long* count, const int32_t (&w)[KU],
-                                                 const int64_t (&s)[KU], const uint32_t (&d)[KU],
-                                                 const bool (&hub)[KU]) {
-  uint32_t nh = 0;
-  uint32_t nk[KU];
+__device__ __forceinline__ void warp_push_rows(QEnt* hq, uint32_t* hs, unsigned long long* count,
+                                               const int32_t (&w)[KU], const int64_t (&s)[KU],
+                                               const uint32_t (&d)[KU], const bool (&hub)[KU]) {
+  uint32_t nr = 0, ns = 0;
 #pragma unroll
   for (int k = 0; k < KU; ++k) {
-    nk[k] = hub[k] ? (d[k] + kChunk - 1) / kChunk : 0u;
-    nh += nk[k];
+    nr += hub[k] ? 1u : 0u;
+    ns += hub[k] ? (d[k] + kChunk - 1) / kChunk : 0u;
   }
-  const uint32_t ih = rb::warp_incl_scan(nh);
-  const uint32_t th = __shfl_sync(RB_FULL, ih, 31);
-  if (th == 0) return;
-  const uint32_t lane = rb::lane_id();
+  const uint32_t ir = rb::warp_incl_scan(nr);
+  const uint32_t tr = __shfl_sync(RB_FULL, ir, 31);
+  if (tr == 0) return;
+  const uint32_t is = rb::warp_incl_scan(ns);
+  const uint32_t ts = __shfl_sync(RB_FULL, is, 31);
   unsigned long long b = 0;
-  if (lane == 31) b = atomicAdd(count, (unsigned long long)th);
-  const unsigned long long bh = __shfl_sync(RB_FULL, b, 31);
-  for (uint32_t r = 0; r < th; r += 32) {
-    const uint32_t idx = r + lane;
-    const bool act = idx < th;
-    const uint32_t j = rb::warp_upper_bound(ih, act ? idx : th - 1);
-    uint32_t local = (act ? idx : th - 1) - (__shfl_sync(RB_FULL, ih, j) - __shfl_sync(RB_FULL, nh, j));
-    int32_t ew = 0;
-    int64_t es = 0;
-    uint32_t ed = 0;
-    bool got = false;
+  if (rb::lane_id() == 31) b = atomicAdd(count, ((unsigned long long)tr << 40) | ts);
+  b = __shfl_sync(RB_FULL, b, 31);
+  uint64_t r = (b >> 40) + ir - nr;
+  uint32_t sl = (uint32_t)(b & kSliceMask) + is - ns;
 #pragma unroll
-    for (int k = 0; k < KU; ++k) {
-      const uint32_t cnt = __shfl_sync(RB_FULL, nk[k], j);
-      const int32_t wk = __shfl_sync(RB_FULL, w[k], j);
-      const int64_t sk = rb::shfl_i64(s[k], j);
-      const uint32_t dk = __shfl_sync(RB_FULL, d[k], j);
-      if (!got && local < cnt) {
-        got = true;
-        ew = wk;
-        es = sk + (int64_t)local * kChunk;
-        ed = min(kChunk, dk - local * kChunk);
-      } else if (!got) {
-        local -= cnt;
-      }
-    }
-    if (act) {
-      QEnt e;
-      e.s = es;
-      e.v = ew;
-      e.d = (int32_t)ed;
-      hq[bh + idx] = e;
-    }
+  for (int k = 0; k < KU; ++k) {
+    if (!hub[k]) continue;
+    QEnt e;
+    e.s = s[k];
+    e.v = w[k];
+    e.d = (int32_t)d[k];
+    hq[r] = e;
+    hs[r] = sl;
+    ++r;
+    sl += (d[k] + kChunk - 1) / kChunk;
   }
+}
+
+// The hub row holding slice i (warp-uniform i < total slices): the last row
+// whose first slice <= i, by a 32-ary warp search over hs.
+__device__ __forceinline__ uint64_t row_of_slice(const uint32_t* hs, uint64_t nrows, uint64_t i) {
+  const uint32_t lane = rb::lane_id();
+  uint64_t lo = 0, hi = nrows;
+  while (hi - lo > 32) {
+    const uint64_t step = (hi - lo + 31) / 32;
+    const uint64_t idx = lo + lane * step;
+    const bool le = idx < hi && (uint64_t)__ldcg(hs + idx) <= i;
+    const uint32_t m = __ballot_sync(RB_FULL, le);  // lane 0 always qualifies
+    lo += (uint64_t)(31 - __clz(m)) * step;
+    hi = min(lo + step, hi);
+  }
+  const uint64_t idx = lo + lane;
+  const uint32_t m = __ballot_sync(RB_FULL, idx < hi && (uint64_t)__ldcg(hs + idx) <= i);
+  return lo + (31 - __clz(m));
 }
 
 // Top-down phase A: the frontier rows straight from the bitmap.  Rows with
@@ -399,7 +407,7 @@ __device__ __forceinline__ void warp_push_slices(QEnt* hq, unsigned long long* c
 // edge-balanced across the warp (4 edges per lane per step), hub rows are
 // appended as 256-edge slices for phase B.
 // The rows of a warp's shared-memory list lst[0, tot), 4 per lane per round.
-__device__ __forceinline__ void td_list(const TdCtx& c, const uint32_t* lst, uint32_t tot, QEnt* hq,
+__device__ __forceinline__ void td_list(const TdCtx& c, const uint32_t* lst, uint32_t tot, QEnt* hq, uint32_t* hs,
                                         unsigned long long* hq_count, Acc& acc) {
   const KParams& p = *c.p;
   const uint32_t lane = rb::lane_id();
@@ -476,7 +484,7 @@ __device__ __forceinline__ void td_list(const TdCtx& c, const uint32_t* lst, uin
       }
       td_claim<kTdUnroll>(c, vv, w, act, acc);
     }
-    warp_push_slices<kUB>(hq, hq_count, v, s0, d, hub);
+    warp_push_rows<kUB>(hq, hs, hq_count, v, s0, d, hub);
   }
 }
 
@@ -488,7 +496,8 @@ __device__ __forceinline__ void td_list(const TdCtx& c, const uint32_t* lst, uin
 // batch ahead, its words in flight).  The nonzero words of a batch are
 // compacted into the warp's shared-memory list, at most 256 rows per round
 // (popc + warp scan + a loop over each lane's set bits).
-RB_LEVEL_FN void td_rows_words(const TdCtx& c, QEnt* hq, unsigned long long* hq_count, Acc& acc, uint32_t* lst,
+RB_LEVEL_FN void td_rows_words(const TdCtx& c, QEnt* hq, uint32_t* hs, unsigned long long* hq_count, Acc& acc,
+                               uint32_t* lst,
                               uint32_t* s_next) {
   const KParams& p = *c.p;
   const uint32_t lane = rb::lane_id();
@@ -522,7 +531,7 @@ RB_LEVEL_FN void td_rows_words(const TdCtx& c, QEnt* hq, unsigned long long* hq_
         x = 0u;
       }
       __syncwarp();
-      td_list(c, lst, tot, hq, hq_count, acc);
+      td_list(c, lst, tot, hq, hs, hq_count, acc);
     }
   }
 }
@@ -531,7 +540,8 @@ RB_LEVEL_FN void td_rows_words(const TdCtx& c, QEnt* hq, unsigned long long* hq_
 // the nonzero summary (each bit covers one bitmap word, a byte one 256-vertex
 // item) strided over the whole range, so one load skips 32 empty items; a
 // nonzero item is compacted into the warp's list (lane l owns byte l).
-RB_LEVEL_FN void td_rows_items(const TdCtx& c, const uint8_t* nzcur, QEnt* hq, unsigned long long* hq_count,
+RB_LEVEL_FN void td_rows_items(const TdCtx& c, const uint8_t* nzcur, QEnt* hq, uint32_t* hs,
+                               unsigned long long* hq_count,
                               Acc& acc, uint32_t* lst) {
   const KParams& p = *c.p;
   const uint32_t lane = rb::lane_id();
@@ -563,7 +573,7 @@ RB_LEVEL_FN void td_rows_items(const TdCtx& c, const uint8_t* nzcur, QEnt* hq, u
         byte &= byte - 1;
       }
       __syncwarp();
-      td_list(c, lst, tot, hq, hq_count, acc);
+      td_list(c, lst, tot, hq, hs, hq_count, acc);
     }
   }
 }
@@ -605,51 +615,82 @@ __device__ void count_next(const KParams& p, uint32_t* fnext, uint8_t* nznext, A
 }
 
 // Top-down phase B: hub slices, one warp item each (8 edges per lane).
-RB_LEVEL_FN void td_hubs(const TdCtx& c, const QEnt* hq, uint64_t nh, Acc& acc) {
-  // Software-pipelined over the warp's slices: while slice i is probed and
-  // claimed, the columns of slice i+1 and the entry of slice i+2 are in
-  // flight (a slice is otherwise a chain entry -> columns -> probes).
+RB_LEVEL_FN void td_hubs(const TdCtx& c, const QEnt* hq, const uint32_t* hs, uint64_t nrows, uint64_t nh,
+                         Acc& acc) {
+#if defined(RB_TD_EXPERIMENT) && RB_TD_EXPERIMENT == 3
+  if (c.defer) return;
+#endif
+  // Warp g takes the contiguous slices [g*K, (g+1)*K): one row search per
+  // warp, then the rows are walked in order (each warp streams its own part
+  // of the column array).  Software-pipelined: the columns of the next slice
+  // are in flight while the current one is probed and claimed.
   const KParams& p = *c.p;
   const uint32_t lane = rb::lane_id();
   const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
-  uint64_t item = warp_slot();
-  if (item >= nh) return;
-  auto entry = [&](uint64_t i) -> QEnt {
-    if (i < nh) return ld_qent(hq + i);
-    QEnt z;
-    z.s = 0;
-    z.v = 0;
-    z.d = 0;
-    return z;
-  };
-  auto columns = [&](const QEnt& e, int32_t (&w)[kChunkPerLane]) {
+  const uint64_t K = (nh + nwarps - 1) / nwarps;
+  const uint64_t i0 = warp_slot() * K;
+  if (i0 >= nh) return;
+  uint32_t left = (uint32_t)min(K, nh - i0);  // slices still to process
+  // current slice: row entry `row` (index r), edges [row.s + o, row.s + o + 256) of it
+  int32_t w[kChunkPerLane];
+  auto columns = [&](const QEnt& e, int32_t (&x)[kChunkPerLane]) {
 #pragma unroll
     for (int k = 0; k < kChunkPerLane; ++k) {
       const int32_t j = (int32_t)lane + 32 * k;
-      w[k] = j < e.d ? rb::ldg_i32(p.td_col + e.s + j) : -1;
+      x[k] = j < e.d ? rb::ldg_i32(p.td_col + e.s + j) : -1;
     }
   };
-  QEnt e = entry(item);
-  QEnt e2 = entry(item + nwarps);
-  int32_t w[kChunkPerLane];
-  columns(e, w);
+  // the row's remaining edges after the current slice, and the next row index
+  int64_t rest;   // edges of the current row after this slice
+  uint64_t rnext;  // index of the next row
+  QEnt cur;
+  {
+    const uint64_t r0 = row_of_slice(hs, nrows, i0);
+    const QEnt row = ld_qent(hq + r0);
+    const int64_t off = (int64_t)(i0 - __ldcg(hs + r0)) * kChunk;
+    cur.s = row.s + off;
+    cur.v = row.v;
+    cur.d = (int32_t)min((int64_t)kChunk, (int64_t)row.d - off);
+    rest = (int64_t)row.d - off - cur.d;
+    rnext = r0 + 1;
+  }
+  columns(cur, w);
   while (true) {
-    const QEnt e3 = entry(item + 2 * nwarps);
+    // descriptor of the next slice (same row, or the start of the next row)
+    QEnt nx;
+    nx.s = 0;
+    nx.v = 0;
+    nx.d = 0;
+    int64_t nrest = 0;
+    if (left > 1) {
+      if (rest > 0) {
+        nx.s = cur.s + cur.d;
+        nx.v = cur.v;
+        nx.d = (int32_t)min((int64_t)kChunk, rest);
+        nrest = rest - nx.d;
+      } else {
+        const QEnt row = ld_qent(hq + rnext);
+        ++rnext;
+        nx.s = row.s;
+        nx.v = row.v;
+        nx.d = min((int32_t)kChunk, row.d);
+        nrest = (int64_t)row.d - nx.d;
+      }
+    }
     int32_t w2[kChunkPerLane];
-    columns(e2, w2);
-    if (lane == 0) acc.scan += (unsigned long long)e.d;
+    columns(nx, w2);
+    if (lane == 0) acc.scan += (unsigned long long)cur.d;
     int32_t vv[kChunkPerLane];
     bool act[kChunkPerLane];
 #pragma unroll
     for (int k = 0; k < kChunkPerLane; ++k) {
-      vv[k] = e.v;
+      vv[k] = cur.v;
       act[k] = w[k] >= 0;
     }
     td_claim<kChunkPerLane>(c, vv, w, act, acc);
-    item += nwarps;
-    if (item >= nh) break;
-    e = e2;
-    e2 = e3;
+    if (--left == 0) break;
+    cur = nx;
+    rest = nrest;
 #pragma unroll
     for (int k = 0; k < kChunkPerLane; ++k) w[k] = w2[k];
   }
@@ -965,8 +1006,12 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* warp_t
   return warp_tot[w] + incl - x;
 }
 
-// Runs in CTA 0 only.  On return the state variables describe the first
-// level that is not run solo (or the end of the traversal).
+// Runs in CTA 0 only, with the frontier of level L listed in smem[kSoloCap,
+// kSoloCap + nf) and the buffer fb[(L+2)%3] zero.  On return the state
+// variables describe the first level that is not run solo (or the end of
+// the traversal).  (Tried: re-entering solo mode for the tail levels of a
+// traversal -- their cost is the same chain of dependent misses either way,
+// so the entry pass and barrier made them slower.)
 __device__ __forceinline__ void solo_levels(const KParams& p, uint32_t* smem, SoloShared* sh, uint32_t* warp_tot, int64_t& L,
                             int& dir, int64_t& nf, int64_t& mf, int64_t& mu, int64_t& done, bool& hubs,
                             uint64_t& t_prev, int64_t& reached) {
@@ -976,8 +1021,7 @@ __device__ __forceinline__ void solo_levels(const KParams& p, uint32_t* smem, So
   uint32_t* qn = smem + 2 * kSoloCap;  // frontier of level L+1
   uint32_t* sOff = smem + 3 * kSoloCap;
   int64_t* sS = reinterpret_cast<int64_t*>(smem + 4 * kSoloCap);
-  uint32_t np = 0, nc = 1;
-  if (tid == 0) qc[0] = (uint32_t)p.src;
+  uint32_t np = 0, nc = (uint32_t)nf;
   __syncthreads();
   while (true) {
     const int r0 = (int)(L % 3), r1 = (r0 + 1) % 3, r2 = (r0 + 2) % 3;
@@ -1074,7 +1118,7 @@ __device__ __forceinline__ void solo_levels(const KParams& p, uint32_t* smem, So
       r.t_ns = (int64_t)(t_now - t_prev);
       r.n_next = n_next;
       r.t_queue_ns = 0;
-      r.reserved = dir;  // executed direction (solo levels: top-down)
+      r.reserved = 0;  // executed direction (solo levels: top-down)
       p.rec[done] = r;
       t_prev = t_now;
     }
@@ -1136,6 +1180,7 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
     if (blockIdx.x == 0) {
       uint64_t t0 = globaltimer();
       bool h = false;
+      if (threadIdx.x == 0) (&s_bu_pair[0][0])[kSoloCap] = (uint32_t)p.src;  // the level-0 frontier list
       solo_levels(p, &s_bu_pair[0][0], &s_solo, s_wtot, L, dir, nf, mf, mu, done, h, t0, reached);
       if (threadIdx.x == 0) {
         p.fin->reached = reached;
@@ -1201,7 +1246,7 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
     int xdir = dir;
     if (p.exec_opt) {
       if (2 * mu > p.m_directed) {
-        if (dir == 1 && mf * kExecAlpha <= mu) xdir = 0;
+        if (dir == 1 && mf * p.exec_alpha <= mu) xdir = 0;
       } else {
         const int64_t U = p.n_active > reached ? p.n_active - reached : 0;
         const int64_t t_td = kTdFixPs + nf * kTdRowPs + mf * kTdEdgePs;
@@ -1213,6 +1258,7 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
     Acc acc{0, 0, 0, 0u};
     if (xdir == 0) {
       QEnt* hq = (L & 1) ? p.hq1 : p.hq0;
+      uint32_t* hs = (L & 1) ? p.hs1 : p.hs0;
       TdCtx c;
       c.p = &p;
       c.L = L;
@@ -1228,12 +1274,13 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
         for (uint64_t i = gtid; i < (uint64_t)p.n_words / 4; i += gthreads)
           reinterpret_cast<uint4*>(fnext)[i] = __ldcg(reinterpret_cast<const uint4*>(p.vis) + i);
         rb::grid_barrier(p.bar, nblocks, epoch);
+        if (p.dbg && blockIdx.x == 0 && threadIdx.x == 0 && done < 64) p.dbg[kDbgPhase + done * 8 + 0] = globaltimer();
       }
       // phase A: frontier rows from the bitmap; hub rows become slices in hq
       if (nf >= kDenseFrontier)
-        td_rows_words(c, hq, &in->hq_count, acc, s_bu_pair[threadIdx.x >> 5], &s_bu_next[L & 1]);
+        td_rows_words(c, hq, hs, &in->hq_count, acc, s_bu_pair[threadIdx.x >> 5], &s_bu_next[L & 1]);
       else
-        td_rows_items(c, p.nzcur_ext ? p.nzcur_ext : nz_of(p, r0), hq, &in->hq_count, acc,
+        td_rows_items(c, p.nzcur_ext ? p.nzcur_ext : nz_of(p, r0), hq, hs, &in->hq_count, acc,
                       s_bu_pair[threadIdx.x >> 5]);
       if (hubs) {  // phase B only if some frontier row has more than kLightDeg edges
         {
@@ -1241,11 +1288,15 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
           rb::grid_barrier_fetch<1>(p.bar, nblocks, epoch, src, s_ctr);
         }
         if (blockIdx.x == 0 && threadIdx.x == 32) t_queue = globaltimer() - t_prev;
-        td_hubs(c, hq, s_ctr[0], acc);
+        if (p.dbg && blockIdx.x == 0 && threadIdx.x == 0 && done < 64) p.dbg[kDbgPhase + done * 8 + 1] = globaltimer();
+        td_hubs(c, hq, hs, s_ctr[0] >> 40, s_ctr[0] & kSliceMask, acc);
       }
+      if (p.dbg && blockIdx.x == 0 && threadIdx.x == 0 && done < 64) p.dbg[kDbgPhase + done * 8 + 2] = globaltimer();
       if (c.defer) {
         rb::grid_barrier(p.bar, nblocks, epoch);  // every claim of the level has landed
+        if (p.dbg && blockIdx.x == 0 && threadIdx.x == 0 && done < 64) p.dbg[kDbgPhase + done * 8 + 3] = globaltimer();
         count_next(p, fnext, nz_of(p, r1), acc);
+        if (p.dbg && blockIdx.x == 0 && threadIdx.x == 0 && done < 64) p.dbg[kDbgPhase + done * 8 + 4] = globaltimer();
       }
     } else {
       const uint32_t wib = threadIdx.x >> 5;
@@ -1485,6 +1536,8 @@ extern "C" int rb_bfs_create_part(const int64_t* d_row_starts, const int32_t* d_
   if (const char* env = getenv("RB_DEFER_MF")) h->defer_mf = atoll(env);
   h->kp.probe_mf = h->probe_mf;  // also seen by rb_bfs_dist_level (which copies kp)
   h->kp.defer_mf = h->defer_mf;
+  h->kp.exec_alpha = kExecAlpha;
+  if (const char* env = getenv("RB_EXEC_ALPHA")) h->kp.exec_alpha = atoll(env);
   cudaEventCreate(&h->ev_start);
   cudaEventCreate(&h->ev_end);
   if (const char* env = getenv("RB_DEBUG")) h->kp.debug = atoi(env);
@@ -1518,6 +1571,8 @@ extern "C" int rb_bfs_create_part(const int64_t* d_row_starts, const int32_t* d_
   RB_ALLOC(h->vinfo, (size_t)n_dev * sizeof(VInfo));
   RB_ALLOC(k.hq0, nhub * sizeof(QEnt));
   RB_ALLOC(k.hq1, nhub * sizeof(QEnt));
+  RB_ALLOC(k.hs0, nhub * sizeof(uint32_t));
+  RB_ALLOC(k.hs1, nhub * sizeof(uint32_t));
 
   RB_ALLOC(k.parent, (size_t)n_dev * 4);
   RB_ALLOC(h->hot, (size_t)n_dev * sizeof(int2));
@@ -1554,6 +1609,11 @@ extern "C" int rb_bfs_create_part(const int64_t* d_row_starts, const int32_t* d_
     make_vinfo<<<1024, 256>>>(part->d_td_row_starts, part->d_td_col, part->n_glob, h->td_vinfo);
     k.td_vinfo = h->td_vinfo;
     k.td_col = part->d_td_col;
+    if (cudaMemcpy(&k.td_m, part->d_td_row_starts + part->n_glob, 8, cudaMemcpyDeviceToHost) != cudaSuccess) {
+      rb_set_error("rb_bfs_create: reading the transpose slice size failed");
+      rb_bfs_destroy(h);
+      return RB_ERR_CUDA;
+    }
     k.td_rs = part->d_td_row_starts;
     h->n_glob = part->n_glob;
   } else {
@@ -1561,6 +1621,7 @@ extern "C" int rb_bfs_create_part(const int64_t* d_row_starts, const int32_t* d_
     k.n_words_glob = h->n_words;
     k.td_vinfo = h->vinfo;
     k.td_col = d_col;
+    k.td_m = params->m_directed;
     k.td_rs = d_row_starts;
     h->n_glob = n_dev;
   }
@@ -1602,7 +1663,7 @@ extern "C" int rb_bfs_create_part(const int64_t* d_row_starts, const int32_t* d_
 extern "C" int rb_bfs_destroy(rb_bfs* h) {
   if (!h) return RB_OK;
   KParams& k = h->kp;
-  void* ptrs[] = {k.vis, k.fb0, k.fb1, k.fb2, h->vis_template, h->pad_mask, k.hq0, k.hq1, k.parent,
+  void* ptrs[] = {k.vis, k.fb0, k.fb1, k.fb2, h->vis_template, h->pad_mask, k.hq0, k.hq1, k.hs0, k.hs1, k.parent,
                   k.level, k.slots, k.bar, k.rec, k.fin, k.nz0, k.nz1, k.nz2, h->hot, h->vinfo, k.dbg, h->td_vinfo};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -1672,6 +1733,7 @@ static int launch(rb_bfs* h, cudaStream_t s, int64_t level0, int64_t dir0, int64
   kp.reached0 = reached0;
   kp.probe_mf = h->probe_mf;
   kp.defer_mf = h->defer_mf;
+  kp.exec_alpha = h->kp.exec_alpha;
   void* args[] = {&kp};
   cudaError_t e;
   e = cudaLaunchCooperativeKernel(bfs_kernel(h), dim3(h->blocks), dim3(kThreads), args, 0, s);

@@ -28,7 +28,33 @@ with rb.BfsEngine(g2, rb.BfsParams()) as eng:
     eng.run_device(s)
     flush.zero_()
     t, levels = eng.run_device(s)
-print(f"root {s} (index {a.index}): {t * 1e6:.1f} us")
-for r in levels:
-    print(f"  L{r.level} {r.direction[0].upper()}{(r.executed_direction or r.direction)[0].upper()} n_f={r.n_f} "
-          f"m_f={r.m_f} scanned={r.scanned_edges} t={r.wall_time * 1e6:.1f} us (phase A {r.queue_time * 1e6:.1f} us)")
+    print(f"root {s} (index {a.index}): {t * 1e6:.1f} us")
+    for r in levels:
+        print(f"  L{r.level} {r.direction[0].upper()}{(r.executed_direction or r.direction)[0].upper()} n_f={r.n_f} "
+              f"m_f={r.m_f} scanned={r.scanned_edges} t={r.wall_time * 1e6:.1f} us (phase A {r.queue_time * 1e6:.1f} us)")
+    if os.environ.get("RB_DEBUG_TS"):  # CTA 0 sub-phase stamps of each grid level (solo levels excluded)
+        import ctypes
+
+        import numpy as np
+        from paper_2012_10026_b200 import _lib
+
+        buf = np.zeros(65536 + 64 * 148 * 32, np.uint64)
+        nb = ctypes.c_int(0)
+        _lib.check(_lib.lib().rb_bfs_debug_timestamps(eng._dev.h, buf.ctypes.data_as(ctypes.c_void_p), buf.size,
+                                                      ctypes.byref(nb)))
+        ts = buf[: 64 * 4 * nb.value].reshape(64, nb.value, 4).astype(np.int64)
+        ph = buf[60000: 60000 + 64 * 8].reshape(64, 8).astype(np.int64)
+        for L in range(len(levels)):
+            t0 = ts[L, 0, 0]
+            if t0 == 0:
+                continue
+            marks = " ".join(f"p{j}={(ph[L, j] - t0) / 1e3:.1f}" for j in range(8) if ph[L, j] > t0)
+            print(f"  stamps L{L}: work end {(ts[L, 0, 1] - t0) / 1e3:.1f} us  {marks}")
+            if L + 1 < 64 and ph[L + 1, 5] > t0:  # a solo tail entered after this level
+                print(f"    tail entry after L{L}: " + " ".join(f"p{j}={(ph[L + 1, j] - t0) / 1e3:.1f}" for j in (5, 6, 7)))
+                wt = buf[65536 + (L + 1) * nb.value * 32: 65536 + (L + 2) * nb.value * 32].astype(np.int64)
+                wt = (wt - t0) / 1e3
+                order = np.argsort(-wt)[:8]
+                print("    slowest warps (cta, warp, end us):", [(int(i // 32), int(i % 32), round(float(wt[i]), 1)) for i in order])
+                raw = buf[65536 + (L + 1) * nb.value * 32: 65536 + (L + 2) * nb.value * 32]
+                print("    warps without a stamp:", int((raw == 0).sum()), "of", raw.size, " min end", round(float(wt.min()), 1))
