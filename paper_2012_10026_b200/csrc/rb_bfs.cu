@@ -275,15 +275,6 @@ __device__ __forceinline__ void td_claim(const TdCtx& c, const int32_t (&v)[KU],
   int32_t wl[KU];
 #pragma unroll
   for (int k = 0; k < KU; ++k) wl[k] = w[k] - (int32_t)p.v_lo;
-#ifdef RB_TD_EXPERIMENT  // timing experiments only (wrong results): 1 = columns only, 2 = + probes
-  if (c.defer) {
-    uint32_t x = 0;
-#pragma unroll
-    for (int k = 0; k < KU; ++k) x += (RB_TD_EXPERIMENT >= 2 && act[k]) ? ld_bits(p.vis + (wl[k] >> 5)) : (uint32_t)wl[k];
-    if (x == 0x12345678u) p.parent[0] = (int32_t)x;
-    return;
-  }
-#endif
   if (c.defer) {
     // Big levels: no atomic return trip and no per-winner degree load.  Every
     // frontier vertex adjacent to an unvisited w is a valid parent of w, so
@@ -385,8 +376,12 @@ __device__ __forceinline__ void warp_push_rows(QEnt* hq, uint32_t* hs, unsigned 
 }
 
 // The hub row holding slice i (warp-uniform i < total slices): the last row
-// whose first slice <= i, by a 32-ary warp search over hs.
-__device__ __forceinline__ uint64_t row_of_slice(const uint32_t* hs, uint64_t nrows, uint64_t i) {
+// whose first slice <= i, by a 32-ary warp search over hs.  The final step
+// loads the candidate rows' entries together with their first slices, so a
+// level with <= 32 hub rows pays one round trip.  Returns the row entry and
+// sets *first to its first slice and *r to its index.
+__device__ __forceinline__ QEnt row_of_slice(const QEnt* hq, const uint32_t* hs, uint64_t nrows, uint64_t i,
+                                             uint32_t* first, uint64_t* r) {
   const uint32_t lane = rb::lane_id();
   uint64_t lo = 0, hi = nrows;
   while (hi - lo > 32) {
@@ -398,8 +393,19 @@ __device__ __forceinline__ uint64_t row_of_slice(const uint32_t* hs, uint64_t nr
     hi = min(lo + step, hi);
   }
   const uint64_t idx = lo + lane;
-  const uint32_t m = __ballot_sync(RB_FULL, idx < hi && (uint64_t)__ldcg(hs + idx) <= i);
-  return lo + (31 - __clz(m));
+  const bool in = idx < hi;
+  const uint32_t h = in ? __ldcg(hs + idx) : 0xffffffffu;
+  const int4 q = in ? __ldcg(reinterpret_cast<const int4*>(hq + idx)) : make_int4(0, 0, 0, 0);
+  const uint32_t m = __ballot_sync(RB_FULL, in && (uint64_t)h <= i);
+  const int j = 31 - __clz(m);
+  *first = __shfl_sync(RB_FULL, h, j);
+  *r = lo + j;
+  QEnt e;
+  e.s = (long long)(((unsigned long long)(uint32_t)__shfl_sync(RB_FULL, q.y, j) << 32) |
+                    (uint32_t)__shfl_sync(RB_FULL, q.x, j));
+  e.v = __shfl_sync(RB_FULL, q.z, j);
+  e.d = __shfl_sync(RB_FULL, q.w, j);
+  return e;
 }
 
 // Top-down phase A: the frontier rows straight from the bitmap.  Rows with
@@ -617,9 +623,6 @@ __device__ void count_next(const KParams& p, uint32_t* fnext, uint8_t* nznext, A
 // Top-down phase B: hub slices, one warp item each (8 edges per lane).
 RB_LEVEL_FN void td_hubs(const TdCtx& c, const QEnt* hq, const uint32_t* hs, uint64_t nrows, uint64_t nh,
                          Acc& acc) {
-#if defined(RB_TD_EXPERIMENT) && RB_TD_EXPERIMENT == 3
-  if (c.defer) return;
-#endif
   // Warp g takes the contiguous slices [g*K, (g+1)*K): one row search per
   // warp, then the rows are walked in order (each warp streams its own part
   // of the column array).  Software-pipelined: the columns of the next slice
@@ -645,9 +648,10 @@ RB_LEVEL_FN void td_hubs(const TdCtx& c, const QEnt* hq, const uint32_t* hs, uin
   uint64_t rnext;  // index of the next row
   QEnt cur;
   {
-    const uint64_t r0 = row_of_slice(hs, nrows, i0);
-    const QEnt row = ld_qent(hq + r0);
-    const int64_t off = (int64_t)(i0 - __ldcg(hs + r0)) * kChunk;
+    uint32_t first;
+    uint64_t r0;
+    const QEnt row = row_of_slice(hq, hs, nrows, i0, &first, &r0);
+    const int64_t off = (int64_t)(i0 - first) * kChunk;
     cur.s = row.s + off;
     cur.v = row.v;
     cur.d = (int32_t)min((int64_t)kChunk, (int64_t)row.d - off);
