@@ -56,7 +56,7 @@
 namespace {
 
 #ifndef RB_THREADS
-#define RB_THREADS 1024
+#define RB_THREADS 768  // 24 warps x 80 registers: measured best (1024 x 64 spills in the bottom-up loop; s22 -8%, s26 -6%, Chung-Lu -9%)
 #endif
 constexpr int kThreads = RB_THREADS;
 // Level bodies are separate (non-inlined) functions: each gets its own
@@ -985,7 +985,7 @@ __device__ __forceinline__ void block_add3(unsigned long long* red, const Acc& a
 // holds exactly the frontier of level L-1, whose bits are cleared from its
 // list.  Entry only at the start of a traversal (level 0, frontier {src}).
 
-constexpr int kSoloCap = 1024;     // frontier vertices held in shared memory
+constexpr int kSoloCap = kThreads < 1024 ? kThreads : 1024;  // frontier vertices held in shared memory (one row per thread)
 constexpr int64_t kSoloMf = 4096;  // frontier edges of a solo level
 
 struct SoloShared {
