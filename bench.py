@@ -456,7 +456,7 @@ def run_ours(args):
                 "api": "BfsEngine.run(source) -> BfsResult with host predecessor"},
         "validation": {"roots": n_val, "passed": n_ok,
                        "method": "GPU Validator: the 5 rules of validate.py (tree edges, levels, spans, coverage)"},
-        "gpu_launches": int(len(my) * 2),  # bfs_seed + bfs_persistent per root
+        "gpu_launches": int(len(my) * 2),  # bfs_reset_all + bfs_persistent per root
         "clocks": clk.summary(),
         "timed_wall_ms": wall_ms,
     }

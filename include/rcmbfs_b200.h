@@ -149,6 +149,16 @@ int rb_bfs_traverse(rb_bfs* h, void* stream);
 /* Device time of the last traversal (all of its launches), seconds. */
 int rb_bfs_elapsed(rb_bfs* h, double* seconds);
 /* Copy results; parents/levels cover [0,n_dev); n_records <= cap. */
+/* Asynchronous result path (BfsEngine.run, engine.py:518-604): enqueue the
+ * copies of the launch state (rb_bfs_state_bytes() bytes) and of the first
+ * `cap` level records behind the traversal on `stream`, without waiting.
+ * After the caller synchronizes the stream, rb_bfs_complete() returns 0 and
+ * the record count when that launch finished the traversal, or 1 when the
+ * caller must drain with rb_bfs_results (continuation launches). */
+int rb_bfs_results_async(rb_bfs* h, void* h_state, rb_level_record* h_records, int64_t cap, void* stream);
+int rb_bfs_complete(rb_bfs* h, const void* h_state, const rb_level_record* h_records, int64_t cap,
+                    int64_t* n_records);
+size_t rb_bfs_state_bytes(void);
 int rb_bfs_results(rb_bfs* h, int32_t* d_or_h_parent, int32_t* d_or_h_level, rb_level_record* h_records,
                    int64_t cap, int64_t* n_records, void* stream);
 /* One step from an explicit state (top_down_step / bottom_up_step,

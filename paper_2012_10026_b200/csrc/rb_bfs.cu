@@ -1373,6 +1373,31 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
   }
 }
 
+// Per-root reset in one launch (engine.py:526-539): parents (and levels)
+// -1, frontier bitmaps and summaries 0, visited = the isolated/padding
+// template, counters 0, and the source seeded by the thread that owns it.
+__global__ void bfs_reset_all(KParams p, const uint32_t* vis_template, int64_t src) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t i = t0; i < p.n_dev; i += stride) {
+    p.parent[i] = i == src ? (int32_t)src : -1;
+    if (p.level) p.level[i] = i == src ? 0 : -1;
+  }
+  const int64_t sw = src >> 5;
+  const uint32_t sb = 1u << (src & 31);
+  for (int64_t i = t0; i < p.n_words; i += stride) {
+    p.fb0[i] = i == sw ? sb : 0u;
+    p.fb1[i] = 0u;
+    p.fb2[i] = 0u;
+    p.nz0[i] = i == sw ? 1u : 0u;
+    p.nz1[i] = 0u;
+    p.nz2[i] = 0u;
+    p.vis[i] = __ldg(vis_template + i) | (i == sw ? sb : 0u);
+  }
+  if (t0 < (int64_t)(3 * sizeof(Slot) / 8)) reinterpret_cast<unsigned long long*>(p.slots)[t0] = 0ull;
+  if (t0 < 16) p.bar[t0] = 0u;
+}
+
 // Per-root reset tail: source seeds (engine.py:526-539).
 __global__ void bfs_seed(KParams p, int64_t src) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
@@ -1709,10 +1734,7 @@ extern "C" int rb_bfs_reset(rb_bfs* h, int64_t source, void* stream) {
     return RB_ERR_ARG;
   }
   cudaStream_t s = (cudaStream_t)stream;
-  int rc = reset_common(h, s);
-  if (rc) return rc;
-  RB_CUDA_TRY(cudaMemcpyAsync(h->kp.vis, h->vis_template, (size_t)h->n_words * 4, cudaMemcpyDeviceToDevice, s));
-  bfs_seed<<<1, 32, 0, s>>>(h->kp, source);
+  bfs_reset_all<<<h->sms * 4, 512, 0, s>>>(h->kp, h->vis_template, source);
   RB_CUDA_TRY(cudaGetLastError());
   h->source = source;
   h->recs.clear();
@@ -1801,6 +1823,37 @@ extern "C" int rb_bfs_results(rb_bfs* h, int32_t* parent_out, int32_t* level_out
   RB_CUDA_TRY(cudaStreamSynchronize(s));
   return RB_OK;
 }
+
+// Asynchronous result path (BfsEngine.run): enqueue the copies of the launch
+// state and the first `cap` level records into caller-owned (pinned) host
+// memory behind the traversal; nothing waits.  After the caller has
+// synchronized the stream, rb_bfs_complete() accepts the host copies when the
+// single launch finished the traversal (returns 0) -- else it returns 1 and
+// the caller drains with rb_bfs_results (very deep graphs: continuations).
+extern "C" int rb_bfs_results_async(rb_bfs* h, void* h_state, rb_level_record* h_records, int64_t cap,
+                                    void* stream) {
+  if (!h || !h_state || (cap > 0 && !h_records)) return RB_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  RB_CUDA_TRY(cudaMemcpyAsync(h_state, h->kp.fin, sizeof(Final), cudaMemcpyDeviceToHost, s));
+  if (cap > 0)
+    RB_CUDA_TRY(cudaMemcpyAsync(h_records, h->kp.rec, (size_t)(cap < kRecCap ? cap : kRecCap) * sizeof(rb_level_record),
+                                cudaMemcpyDeviceToHost, s));
+  return RB_OK;
+}
+
+extern "C" int rb_bfs_complete(rb_bfs* h, const void* h_state, const rb_level_record* h_records, int64_t cap,
+                               int64_t* n_records) {
+  if (!h || !h_state || !n_records) return RB_ERR_ARG;
+  Final f;
+  memcpy(&f, h_state, sizeof(Final));
+  if (!h->launched || f.nf > 0 || f.levels_done > cap) return 1;
+  h->recs.assign(h_records, h_records + f.levels_done);
+  h->launched = false;
+  *n_records = f.levels_done;
+  return RB_OK;
+}
+
+extern "C" size_t rb_bfs_state_bytes(void) { return sizeof(Final); }
 
 extern "C" int rb_bfs_step(rb_bfs* h, int direction, const uint32_t* d_visited_words,
                            const uint32_t* d_frontier_words, const int32_t* d_parent_in, uint32_t* d_visited_out,
