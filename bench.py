@@ -391,7 +391,9 @@ def run_ours(args):
 
     # ---- e2e through the public API: BfsEngine.run -> host predecessor array
     e2e_teps = []
-    for j in my[: min(len(my), 16)]:
+    for j in my[:3]:  # warm the host path (pinned staging buffers, result-array pool of the allocator)
+        eng.run(int(roots[j]))
+    for j in my[: min(len(my), 32)]:
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         res = eng.run(int(roots[j]))
