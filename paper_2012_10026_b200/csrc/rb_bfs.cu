@@ -1160,7 +1160,12 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
   __shared__ uint32_t s_bu_next[2];  // bottom-up: next step of this CTA (level parity)
   __shared__ SoloShared s_solo;
   __shared__ uint32_t s_wtot[32];
-  if (threadIdx.x == 0) s_bu_next[0] = s_bu_next[1] = 0u;
+  if (p.dbg && threadIdx.x == 0 && blockIdx.x == 0) p.dbg[kDbgPhase + 63 * 8 + 0] = globaltimer();  // kernel entry
+  __shared__ long long s_mf0;  // deg(src) at a traversal start (one load per CTA, not per thread)
+  if (threadIdx.x == 0) {
+    s_bu_next[0] = s_bu_next[1] = 0u;
+    if (p.mf0 < 0) s_mf0 = (long long)rb::ld_relaxed_u64((const unsigned long long*)&p.fin->mf);
+  }
   __syncthreads();
   const uint32_t nblocks = gridDim.x;
   const uint64_t gtid = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
@@ -1170,8 +1175,8 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
   int dir = (int)p.dir0;
   int need_compact = (int)p.need_compact0;
   int64_t nf = p.nf0, mf = p.mf0, mu = p.mu0;
-  if (mf < 0) {  // engine.py:536-538
-    mf = rb::ldg_i64(p.rs + p.src + 1) - rb::ldg_i64(p.rs + p.src);
+  if (mf < 0) {  // engine.py:536-538; deg(src) was stored by the reset kernel
+    mf = (int64_t)s_mf0;
     mu = p.m_directed - mf;
   }
   int64_t done = 0;
@@ -1197,15 +1202,25 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
         p.fin->pad = h ? 1 : 0;
       }
     }
-    rb::grid_barrier(p.bar, nblocks, epoch);
-    done = (int64_t)rb::ld_relaxed_u64((const unsigned long long*)&p.fin->levels_done);
-    L = (int64_t)rb::ld_relaxed_u64((const unsigned long long*)&p.fin->L);
-    dir = (int)rb::ld_relaxed_u64((const unsigned long long*)&p.fin->dir);
-    nf = (int64_t)rb::ld_relaxed_u64((const unsigned long long*)&p.fin->nf);
-    mf = (int64_t)rb::ld_relaxed_u64((const unsigned long long*)&p.fin->mf);
-    mu = (int64_t)rb::ld_relaxed_u64((const unsigned long long*)&p.fin->mu);
-    solo_hubs = rb::ld_relaxed_u64((const unsigned long long*)&p.fin->pad) != 0;
-    reached = (int64_t)rb::ld_relaxed_u64((const unsigned long long*)&p.fin->reached);
+    {
+      // the state after the solo levels: thread 0 of each CTA fetches it
+      // into shared memory (all threads loading it would queue on one line)
+      const unsigned long long* const src[8] = {
+          (const unsigned long long*)&p.fin->levels_done, (const unsigned long long*)&p.fin->L,
+          (const unsigned long long*)&p.fin->dir,         (const unsigned long long*)&p.fin->nf,
+          (const unsigned long long*)&p.fin->mf,          (const unsigned long long*)&p.fin->mu,
+          (const unsigned long long*)&p.fin->pad,         (const unsigned long long*)&p.fin->reached};
+      __shared__ unsigned long long s_fin[8];
+      rb::grid_barrier_fetch<8>(p.bar, nblocks, epoch, src, s_fin);
+      done = (int64_t)s_fin[0];
+      L = (int64_t)s_fin[1];
+      dir = (int)s_fin[2];
+      nf = (int64_t)s_fin[3];
+      mf = (int64_t)s_fin[4];
+      mu = (int64_t)s_fin[5];
+      solo_hubs = s_fin[6] != 0;
+      reached = (int64_t)s_fin[7];
+    }
     need_compact = dir == 0;
   }
   int r0 = (int)(L % 3);
@@ -1361,6 +1376,7 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
     ++done;
     r0 = r0 == 2 ? 0 : r0 + 1;
   }
+  if (p.dbg && threadIdx.x == 0 && blockIdx.x == 0) p.dbg[kDbgPhase + 63 * 8 + 1] = globaltimer();  // kernel exit
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     p.fin->levels_done = done;
     p.fin->L = L;
@@ -1396,6 +1412,7 @@ __global__ void bfs_reset_all(KParams p, const uint32_t* vis_template, int64_t s
   }
   if (t0 < (int64_t)(3 * sizeof(Slot) / 8)) reinterpret_cast<unsigned long long*>(p.slots)[t0] = 0ull;
   if (t0 < 16) p.bar[t0] = 0u;
+  if (t0 == 0) p.fin->mf = (long long)(p.rs[src + 1] - p.rs[src]);  // deg(src) for the traversal's first level
 }
 
 // Per-root reset tail: source seeds (engine.py:526-539).

@@ -44,6 +44,10 @@ with rb.BfsEngine(g2, rb.BfsParams()) as eng:
                                                       ctypes.byref(nb)))
         ts = buf[: 64 * 4 * nb.value].reshape(64, nb.value, 4).astype(np.int64)
         ph = buf[60000: 60000 + 64 * 8].reshape(64, 8).astype(np.int64)
+        ent, ext = int(ph[63, 0]), int(ph[63, 1])
+        lev_sum = sum(r.wall_time for r in levels)
+        print(f"  kernel entry->exit {(ext - ent) / 1e3:.1f} us (CTA 0), sum of level times {lev_sum * 1e6:.1f} us, "
+              f"event time {t * 1e6:.1f} us")
         for L in range(len(levels)):
             t0 = ts[L, 0, 0]
             if t0 == 0:
