@@ -99,6 +99,9 @@ constexpr int64_t kBuFixPs = 3000000;   // a bottom-up level: zeroing + barrier
 constexpr int64_t kBuStepPs = 650000;   // per warp step of the bitmap pass (dependent chain)
 constexpr int64_t kBuVertPs = 5;        // per unvisited vertex
 constexpr int64_t kBuCheckPs = 1;       // per neighbour check (bounded by 8 per unvisited vertex)
+constexpr int64_t kBuSparsePs = 2000000; // sparse bottom-up: the list pass (+ collection barrier)
+constexpr int64_t kSparseRatio = 256;   // sparse bottom-up when at most one vertex in 256 is unvisited
+constexpr int64_t kListRatio = 64;      // a bitmap bottom-up level lists its survivors from one in 64 (list capacity)
 constexpr int kK2 = 258;                         // bottom-up: per-lane checks before the warp takes over
 constexpr int kHeavyPerLane = 8;                 // warp-cooperative bottom-up: neighbours per lane per step
 constexpr uint64_t kDbgWarpBase = 65536;  // RB_DEBUG_TS buffer: per-block stamps, then per-warp stamps
@@ -128,7 +131,9 @@ struct Slot {  // per-level counters, triple-buffered by level % 3
   unsigned long long scanned;
   unsigned long long hq_count;  // hub rows << 40 | their 256-edge slices, appended by phase A of the NEXT level
   unsigned long long maxdeg;    // max degree of the next frontier (hub slices needed?)
-  unsigned long long pad1, pad2, pad3;
+  unsigned long long ul_count;  // sparse bottom-up: 1 << 40 (a list was written) | vertices listed by this level
+  unsigned long long pad2;
+  unsigned long long pad3;
 };
 
 struct Final {  // state after a launch (continuation for very deep graphs)
@@ -195,6 +200,9 @@ struct KParams {
   int64_t defer_mf;       // top-down: fire-and-forget claims + count_next from this many frontier edges
   int64_t td_m;           // entries of td_col
   int64_t exec_alpha;     // early levels labelled bottom-up run top-down if m_f * exec_alpha <= m_u
+  int64_t bu_sparse;      // late bottom-up levels with few unvisited vertices run over a list
+  uint32_t* ul0;          // unvisited-vertex lists (alternating by level parity)
+  uint32_t* ul1;
   int64_t src;
   int64_t m_directed;
   int64_t n_active;  // non-isolated vertices in [0, n_dev) (executed-direction cost model)
@@ -746,9 +754,10 @@ __device__ __forceinline__ int32_t bu_heavy(const KParams& p, const uint32_t* fc
   return -1;
 }
 
-template <bool kRev, int KB>
+template <bool kRev, int KB, bool kCollect>
 RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uint32_t* fnext, uint8_t* nznext,
-                         Acc& acc, uint32_t* s_found, uint32_t* s_pair, uint32_t* s_next) {
+                         Acc& acc, uint32_t* s_found, uint32_t* s_pair, uint32_t* s_next, uint32_t* ulist,
+                         unsigned long long* ulist_count) {
   const uint32_t lane = rb::lane_id();
   const uint64_t nw = (uint64_t)p.n_words;
   int32_t* const level_out = p.level;
@@ -938,8 +947,118 @@ RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uin
         p.vis[w0 + k] = vw | fm;
       }
     }
+    if (kCollect) {  // the vertices still unvisited after this level: the next level's sparse list
+      const uint32_t un = lane < (uint32_t)KB ? ~(vw | fm_s[lane]) : 0u;
+      const uint32_t c = __popc(un);
+      const uint32_t incl = rb::warp_incl_scan(c);
+      const uint32_t tot = __shfl_sync(RB_FULL, incl, 31);
+      if (tot) {
+        unsigned long long b = 0;
+        if (lane == 31) b = atomicAdd(ulist_count, (unsigned long long)tot) & kSliceMask;
+        uint32_t pos = (uint32_t)__shfl_sync(RB_FULL, b, 31) + incl - c;
+        for (uint32_t y = un; y; y &= y - 1) ulist[pos++] = (uint32_t)((w0 + lane) * 32 + (__ffs(y) - 1));
+      }
+    }
     __syncwarp();
     acc.scan += checks;
+  }
+}
+
+// Sparse bottom-up (late levels, at most one unvisited vertex in 256): the
+// unvisited vertices are kept in a list (written by the bitmap level before,
+// bu_level<.., kCollect>; each sparse level rewrites its survivors) and
+// checked one per lane -- the hot pair, then the rest of the row in scan
+// order, 8 neighbours per step.  Found vertices set their bits with reds
+// (words are shared between threads here).  Replaces the 8-word warp steps
+// of bu_level, whose bitmap pass costs ~20 us at scale 26 however few
+// vertices are left.
+
+// Check the listed vertices (one per lane); survivors go to `lout`.  Rows
+// are scanned per lane up to kK2 checks, longer ones by the whole warp
+// (bu_heavy), as in bu_level.
+template <bool kRev>
+__device__ void bu_sparse_pass(const KParams& p, int64_t L, const uint32_t* fcur, uint32_t* fnext, uint8_t* nznext,
+                               const uint32_t* lin, uint64_t n, uint32_t* lout, unsigned long long* lcount, Acc& acc) {
+  const uint32_t lane = rb::lane_id();
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  for (uint64_t base = (uint64_t)blockIdx.x * kThreads + (threadIdx.x & ~31u); base < n; base += stride) {
+    const uint64_t t = base + lane;
+    int32_t v = -1, par = -1;
+    uint32_t d = 0, checks = 0;
+    bool live = false;
+    int64_t s0 = 0;
+    if (t < n) {
+      v = (int32_t)__ldcg(lin + t);
+      if (!((ld_bits(p.vis + (v >> 5)) >> (v & 31)) & 1u)) {  // (a top-down level may have found it since)
+        live = true;
+        const int2 h = __ldg(p.hot + v);
+        d = (uint32_t)rb::ldg_i32(p.deg + v);
+        const uint32_t b0 = h.x >= 0 ? ld_bits(fcur + (h.x >> 5)) : 0u;
+        const uint32_t b1 = h.y >= 0 ? ld_bits(fcur + (h.y >> 5)) : 0u;
+        if (h.x >= 0 && ((b0 >> (h.x & 31)) & 1u)) {
+          par = h.x;
+          checks = 1;
+        } else if (h.y >= 0 && ((b1 >> (h.y & 31)) & 1u)) {
+          par = h.y;
+          checks = 2;
+        } else {
+          checks = min(d, 2u);
+          if (d > 2u) {
+            s0 = rb::ldg_i64(p.rs + v);
+            const int64_t e0 = s0 + d;
+            const int64_t lim = d < (uint32_t)kK2 ? d : kK2;
+            for (int64_t t0 = 2; par < 0 && t0 < lim; t0 += 8) {
+              int32_t uu[8];
+              uint32_t bb[8];
+#pragma unroll
+              for (int k = 0; k < 8; ++k)
+                uu[k] = (t0 + k < lim) ? rb::ldg_i32(p.col_bu + bu_idx<kRev>(s0, e0, t0 + k)) : -1;
+#pragma unroll
+              for (int k = 0; k < 8; ++k) bb[k] = uu[k] >= 0 ? ld_bits(fcur + (uu[k] >> 5)) : 0u;
+#pragma unroll
+              for (int k = 0; k < 8; ++k)
+                if (par < 0 && uu[k] >= 0) {
+                  ++checks;
+                  if ((bb[k] >> (uu[k] & 31)) & 1u) par = uu[k];
+                }
+            }
+          }
+        }
+      }
+    }
+    uint32_t hm = __ballot_sync(RB_FULL, live && par < 0 && d > (uint32_t)kK2);
+    while (hm) {
+      const int h = __ffs(hm) - 1;
+      hm &= hm - 1;
+      const int64_t hs = rb::shfl_i64(s0, h);
+      const int64_t he = hs + __shfl_sync(RB_FULL, d, h);
+      int64_t hc = 0;
+      const int32_t hp = bu_heavy<kRev>(p, fcur, hs, he, kK2, &hc);
+      if ((int)lane == h) {
+        checks += (uint32_t)hc;
+        par = hp;
+      }
+    }
+    const bool keep = live && par < 0;
+    if (par >= 0) {
+      const uint32_t bit = 1u << (v & 31);
+      p.parent[v] = par;
+      if (p.level) p.level[v] = (int32_t)(L + 1);
+      red_or(p.vis + (v >> 5), bit);
+      red_or(fnext + (v >> 5), bit);
+      nznext[v >> 5] = 1u;
+      acc.n += 1;
+      acc.deg += d;
+      acc.maxdeg = max(acc.maxdeg, d);
+    }
+    acc.scan += checks;
+    const uint32_t km = __ballot_sync(RB_FULL, keep);
+    if (km) {
+      unsigned long long b = 0;
+      if (lane == 0) b = atomicAdd(lcount, (unsigned long long)__popc(km)) & kSliceMask;  // (bit 40: list valid)
+      b = __shfl_sync(RB_FULL, b, 0);
+      if (keep) lout[b + __popc(km & ((1u << lane) - 1u))] = (uint32_t)v;
+    }
   }
 }
 
@@ -1153,8 +1272,12 @@ __device__ __forceinline__ void solo_levels(const KParams& p, uint32_t* smem, So
 
 template <bool kRev, int KB>
 __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
+  // Sparse bottom-up lists only in the large-graph build (8-word steps): at
+  // scale 22 the tail levels are latency floors either way and the extra
+  // code costs the small-graph kernel ~2% (measured).
+  constexpr bool kSparseOK = KB == 8;
   __shared__ unsigned long long s_red[kWarps * 4];
-  __shared__ unsigned long long s_ctr[4];
+  __shared__ unsigned long long s_ctr[5];  // [4]: the unvisited list of the last level (bit 40: valid | count)
   __shared__ uint32_t s_bu_found[kWarps][kBU];
   __shared__ uint32_t s_bu_pair[kWarps][32 * kBU > kList ? 32 * kBU : kList];
   __shared__ uint32_t s_bu_next[2];  // bottom-up: next step of this CTA (level parity)
@@ -1164,6 +1287,7 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
   __shared__ long long s_mf0;  // deg(src) at a traversal start (one load per CTA, not per thread)
   if (threadIdx.x == 0) {
     s_bu_next[0] = s_bu_next[1] = 0u;
+    s_ctr[4] = 0ull;  // no unvisited list yet
     if (p.mf0 < 0) s_mf0 = (long long)rb::ld_relaxed_u64((const unsigned long long*)&p.fin->mf);
   }
   __syncthreads();
@@ -1263,14 +1387,22 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
     //    but only thousands of vertices are still unvisited: bottom-up wins
     //    5x; the tail frontiers of a few thousand rows go top-down.
     int xdir = dir;
+    bool sparse = false;   // few unvisited vertices left: sparse bottom-up over the previous level's list
+    bool collect = false;  // bitmap bottom-up that lists the survivors (the next level may go sparse)
+    const unsigned long long ul_code = s_ctr[4];  // from the previous level's closing fetch
     if (p.exec_opt) {
       if (2 * mu > p.m_directed) {
         if (dir == 1 && mf * p.exec_alpha <= mu) xdir = 0;
       } else {
         const int64_t U = p.n_active > reached ? p.n_active - reached : 0;
         const int64_t t_td = kTdFixPs + nf * kTdRowPs + mf * kTdEdgePs;
-        const int64_t t_bu = kBuFixPs + (p.n_words / KB) * kBuStepPs / ((int64_t)nblocks * kWarps) + U * kBuVertPs +
-                             min(mu, 8 * U) * kBuCheckPs;
+        if constexpr (kSparseOK) {
+          sparse = p.bu_sparse && (ul_code >> 40) && U * kSparseRatio <= p.n_dev;
+          collect = p.bu_sparse && !sparse && U * kListRatio <= p.n_dev;
+        }
+        const int64_t t_bu = kBuFixPs +
+                             (sparse ? kBuSparsePs : (p.n_words / KB) * kBuStepPs / ((int64_t)nblocks * kWarps)) +
+                             U * kBuVertPs + min(mu, 8 * U) * kBuCheckPs;
         xdir = t_td <= t_bu ? 0 : 1;
       }
     }
@@ -1319,15 +1451,32 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
       }
     } else {
       const uint32_t wib = threadIdx.x >> 5;
-      bu_level<kRev, KB>(p, L, fcur, fnext, nz_of(p, r1), acc, s_bu_found[wib], s_bu_pair[wib], &s_bu_next[L & 1]);
+      uint32_t* const lout = (L & 1) ? p.ul1 : p.ul0;  // the list this level leaves for the next
+      if (kSparseOK && sparse) {  // over the list the previous level left (its survivors go to lout)
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&out->ul_count, 1ull << 40);  // list valid flag
+        bu_sparse_pass<kRev>(p, L, fcur, fnext, nz_of(p, r1), (L & 1) ? p.ul0 : p.ul1, ul_code & kSliceMask, lout,
+                             &out->ul_count, acc);
+      } else if (kSparseOK && collect) {  // bitmap pass that also lists the vertices left unvisited
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&out->ul_count, 1ull << 40);
+        bu_level<kRev, KB, true>(p, L, fcur, fnext, nz_of(p, r1), acc, s_bu_found[wib], s_bu_pair[wib],
+                                 &s_bu_next[L & 1], lout, &out->ul_count);
+      } else
+        bu_level<kRev, KB, false>(p, L, fcur, fnext, nz_of(p, r1), acc, s_bu_found[wib], s_bu_pair[wib],
+                                  &s_bu_next[L & 1], nullptr, nullptr);
     }
     if (p.dbg && (threadIdx.x & 31) == 0 && done < 64)  // RB_DEBUG_TS: per-warp end of work
       p.dbg[kDbgWarpBase + ((uint64_t)done * gridDim.x + blockIdx.x) * kWarps + (threadIdx.x >> 5)] = globaltimer();
     block_add3(s_red, acc, out);
     const uint64_t tB = globaltimer();
     {
-      const unsigned long long* const src[4] = {&out->n_next, &out->deg_next, &out->maxdeg, &out->scanned};
-      rb::grid_barrier_fetch<4>(p.bar, nblocks, epoch, src, s_ctr);
+      if constexpr (kSparseOK) {
+        const unsigned long long* const src[5] = {&out->n_next, &out->deg_next, &out->maxdeg, &out->scanned,
+                                                  &out->ul_count};
+        rb::grid_barrier_fetch<5>(p.bar, nblocks, epoch, src, s_ctr);
+      } else {
+        const unsigned long long* const src[4] = {&out->n_next, &out->deg_next, &out->maxdeg, &out->scanned};
+        rb::grid_barrier_fetch<4>(p.bar, nblocks, epoch, src, s_ctr);
+      }
     }
     if (p.dbg && threadIdx.x == 0 && done < 64) {  // RB_DEBUG_TS: per-block phase timestamps
       const uint64_t tC = globaltimer();
@@ -1584,6 +1733,8 @@ extern "C" int rb_bfs_create_part(const int64_t* d_row_starts, const int32_t* d_
   h->kp.defer_mf = h->defer_mf;
   h->kp.exec_alpha = kExecAlpha;
   if (const char* env = getenv("RB_EXEC_ALPHA")) h->kp.exec_alpha = atoll(env);
+  h->kp.bu_sparse = 1;
+  if (const char* env = getenv("RB_BU_SPARSE")) h->kp.bu_sparse = atoll(env);
   cudaEventCreate(&h->ev_start);
   cudaEventCreate(&h->ev_end);
   if (const char* env = getenv("RB_DEBUG")) h->kp.debug = atoi(env);
@@ -1619,6 +1770,8 @@ extern "C" int rb_bfs_create_part(const int64_t* d_row_starts, const int32_t* d_
   RB_ALLOC(k.hq1, nhub * sizeof(QEnt));
   RB_ALLOC(k.hs0, nhub * sizeof(uint32_t));
   RB_ALLOC(k.hs1, nhub * sizeof(uint32_t));
+  RB_ALLOC(k.ul0, ((size_t)n_dev / kListRatio + 1024) * sizeof(uint32_t));
+  RB_ALLOC(k.ul1, ((size_t)n_dev / kListRatio + 1024) * sizeof(uint32_t));
 
   RB_ALLOC(k.parent, (size_t)n_dev * 4);
   RB_ALLOC(h->hot, (size_t)n_dev * sizeof(int2));
@@ -1709,7 +1862,7 @@ extern "C" int rb_bfs_create_part(const int64_t* d_row_starts, const int32_t* d_
 extern "C" int rb_bfs_destroy(rb_bfs* h) {
   if (!h) return RB_OK;
   KParams& k = h->kp;
-  void* ptrs[] = {k.vis, k.fb0, k.fb1, k.fb2, h->vis_template, h->pad_mask, k.hq0, k.hq1, k.hs0, k.hs1, k.parent,
+  void* ptrs[] = {k.vis, k.fb0, k.fb1, k.fb2, h->vis_template, h->pad_mask, k.hq0, k.hq1, k.hs0, k.hs1, k.ul0, k.ul1, k.parent,
                   k.level, k.slots, k.bar, k.rec, k.fin, k.nz0, k.nz1, k.nz2, h->hot, h->vinfo, k.dbg, h->td_vinfo};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -1777,6 +1930,7 @@ static int launch(rb_bfs* h, cudaStream_t s, int64_t level0, int64_t dir0, int64
   kp.probe_mf = h->probe_mf;
   kp.defer_mf = h->defer_mf;
   kp.exec_alpha = h->kp.exec_alpha;
+  kp.bu_sparse = h->kp.bu_sparse;
   void* args[] = {&kp};
   cudaError_t e;
   e = cudaLaunchCooperativeKernel(bfs_kernel(h), dim3(h->blocks), dim3(kThreads), args, 0, s);

@@ -255,11 +255,14 @@ def test_random_states_all_step_kernels(cuda_ok):
 
 
 @pytest.mark.parametrize("knobs", [{"RB_DEFER_MF": "0"}, {"RB_DEFER_MF": "0", "RB_SOLO": "0"},
-                                   {"RB_EXEC_OPT": "0"}, {"RB_DEFER_MF": "4096", "RB_PROBE_MF": "0"}])
+                                   {"RB_EXEC_OPT": "0"}, {"RB_DEFER_MF": "4096", "RB_PROBE_MF": "0"},
+                                   {"RB_KB": "8"}, {"RB_KB": "8", "RB_BU_SPARSE": "0"},
+                                   {"RB_KB": "8", "RB_EXEC_ALPHA": "1"}])
 def test_engine_knobs_keep_parity(cuda_ok, ocache, monkeypatch, knobs):
     """Execution knobs change HOW a level runs (deferred fire-and-forget claims
     counted from the next-frontier bitmap, solo levels, the executed direction,
-    probing) -- never the levels, the records or tree validity."""
+    probing, the large-graph build with 8-word bottom-up steps and the sparse
+    list levels) -- never the levels, the records or tree validity."""
     for k, v in knobs.items():
         monkeypatch.setenv(k, v)
     for scale, seed in ((14, 3), (16, 1)):
