@@ -4,7 +4,10 @@ sys.path.insert(0, ".")
 import paper_2012_10026_b200 as rb
 from paper_2012_10026_b200 import _lib, engine
 scale = int(sys.argv[1])
-el = rb.kronecker_generate(rb.KroneckerParams(scale=scale), device=True)
+if len(sys.argv) > 2 and sys.argv[2] == "chunglu":
+    el = rb.chunglu_generate(rb.ChungLuParams(n=1 << scale), device=True)
+else:
+    el = rb.kronecker_generate(rb.KroneckerParams(scale=scale), device=True)
 g = rb.build_csr(el); perm, st = rb.rcm(g); g2 = rb.apply_permutation(g, perm)
 roots = rb.sample_sources(g2.device_arrays()[2].cpu().numpy(), 64, 1)
 eng = rb.BfsEngine(g2, rb.BfsParams())
@@ -32,4 +35,5 @@ for r in roots[:16]:
     for a, b, e in evs: e.synchronize(); pt[a:b].copy_(d.pinned[a:b])
     t = tick("chunks", t)
     lv = engine._records_to_levels((_lib.LevelRecordC * nrec.value).from_buffer_copy(d._recs_pin.numpy().tobytes()[: nrec.value * 80])); t = tick("records->levels", t)
+print(f"n={g2.n} n_dev={d.n_dev}")
 for k, v in T.items(): print(f"{k:18s} {1e3*np.median(v):8.3f} ms")
