@@ -142,3 +142,27 @@ def test_product_does_not_import_oracle():
             if f.endswith(".py"):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
+
+
+def test_result_pool_never_hands_out_a_live_buffer():
+    """Large predecessor arrays come from a pool of mappings (engine.fresh_int32):
+    a mapping is reused only after every view of its previous array is gone."""
+    import gc
+
+    from paper_2012_10026_b200 import engine
+
+    n = 9 << 20
+    a = engine.fresh_int32(n)
+    a[:] = 7
+    view = a[100:200]
+    del a
+    gc.collect()
+    b = engine.fresh_int32(n)
+    assert not np.shares_memory(b, view)
+    assert (view == 7).all()
+    b[:] = 1
+    assert (view == 7).all()
+    del view, b
+    gc.collect()
+    c = engine.fresh_int32(n)  # now a pooled (warm) mapping may come back
+    assert c.flags.writeable and c.size == n and c.dtype == np.int32
