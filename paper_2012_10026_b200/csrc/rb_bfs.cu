@@ -843,7 +843,7 @@ RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uin
       const bool h0 = act && hv[k].x >= 0 && ((hb0[k] >> (hv[k].x & 31)) & 1u);
       const bool h1 = act && !h0 && hv[k].y >= 0 && ((hb1[k] >> (hv[k].y & 31)) & 1u);
       const bool found = h0 || h1;
-      checks += h0 ? 1u : (h1 ? 2u : (act ? min(dg[k], 2u) : 0u));
+      checks += act ? (h0 ? 1u : min(dg[k], 2u)) : 0u;  // (a second-neighbour hit implies dg >= 2)
       if (found) par_out[32 * k] = h0 ? hv[k].x : hv[k].y;
       foundm |= (uint32_t)found << k;
       needm |= (uint32_t)(act && !found && dg[k] > 2u) << k;
@@ -937,14 +937,14 @@ RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uin
       __syncwarp();
     }
     // next-frontier words (pre-zeroed), their summary bytes and the visited
-    // words: the warp owns them
-#pragma unroll
-    for (int k = 0; k < KB; ++k) {
-      const uint32_t fm = fm_s[k];
-      if (lane == (uint32_t)k && fm) {
-        fnext[w0 + k] = fm;
-        nznext[w0 + k] = 1u;
-        p.vis[w0 + k] = vw | fm;
+    // words: the warp owns them; lane k < KB writes word k (it holds vis word k)
+    __syncwarp();  // lane 0's (and the continuation's) fm_s updates are visible
+    if (lane < (uint32_t)KB) {
+      const uint32_t fm = fm_s[lane];
+      if (fm) {
+        fnext[w0 + lane] = fm;
+        nznext[w0 + lane] = 1u;
+        p.vis[w0 + lane] = vw | fm;
       }
     }
     if (kCollect) {  // the vertices still unvisited after this level: the next level's sparse list
