@@ -59,22 +59,7 @@ namespace {
 #define RB_THREADS 768  // 24 warps x 80 registers: measured best (1024 x 64 spills in the bottom-up loop; s22 -8%, s26 -6%, Chung-Lu -9%)
 #endif
 constexpr int kThreads = RB_THREADS;
-// Level bodies are separate (non-inlined) functions: each gets its own
-// register allocation under the 64-register cap instead of sharing one with
-// the whole persistent loop (fewer spills in the bottom-up hot loop).
-#ifndef RB_NOINLINE
-#define RB_NOINLINE 0  // measured: separate functions spill across the call ABI (s26 +35%)
-#endif
-#if RB_NOINLINE
-#define RB_LEVEL_FN __device__ __noinline__
-#else
-#define RB_LEVEL_FN __device__
-#endif
-// hot[] layout: 1 = {first neighbour in scan order, degree} (8 B: one load
-// and one probe per unvisited vertex); 0 = {first, second neighbour} + deg[].
-#ifndef RB_HOT1
-#define RB_HOT1 0  // measured: +1 probe-free byte saving loses on the first bottom-up level
-#endif
+#define RB_LEVEL_FN __device__  // (tried __noinline__ level bodies: call-ABI spills, s26 +35%)
 #ifndef RB_MINB
 #define RB_MINB 1
 #endif
@@ -786,35 +771,7 @@ RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uin
     if (!__any_sync(RB_FULL, actm != 0)) continue;
     const int64_t vbase = (int64_t)w0 * 32 + lane;
     const int2* const hot = p.hot + vbase;
-#if !RB_HOT1
     const int32_t* const deg = p.deg + vbase;
-#endif
-#if RB_HOT1
-    // round 1: the scan-first neighbour and the degree from the compact
-    // `hot` side array (8 B per vertex, coalesced) -- all KB loads in flight
-    int2 hv[KB];
-#pragma unroll
-    for (int k = 0; k < KB; ++k) hv[k] = ((actm >> k) & 1u) ? __ldg(hot + 32 * k) : make_int2(-1, 0);
-    uint32_t hb0[KB];
-#pragma unroll
-    for (int k = 0; k < KB; ++k) hb0[k] = hv[k].x >= 0 ? ld_bits(fcur + (hv[k].x >> 5)) : 0u;
-    uint32_t dg[KB];
-    uint32_t foundm = 0, needm = 0, checks = 0, dsum = 0, dmax = 0;
-    int32_t* const par_out = p.parent + vbase;
-#pragma unroll
-    for (int k = 0; k < KB; ++k) {
-      const bool act = (actm >> k) & 1u;
-      dg[k] = (uint32_t)hv[k].y;
-      const bool found = act && hv[k].x >= 0 && ((hb0[k] >> (hv[k].x & 31)) & 1u);
-      checks += (act && dg[k]) ? 1u : 0u;
-      if (found) par_out[32 * k] = hv[k].x;
-      foundm |= (uint32_t)found << k;
-      needm |= (uint32_t)(act && !found && dg[k] > 1u) << k;
-      dsum += found ? dg[k] : 0u;
-      dmax = max(dmax, found ? dg[k] : 0u);
-    }
-    constexpr int kFirst = 1;  // checks done by round 1 on a continuing row
-#else
     // round 1: the two scan-first neighbours from the compact `hot` side
     // array (8 B per vertex, coalesced) -- all KB loads in flight
     int2 hv[KB];
@@ -851,7 +808,6 @@ RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uin
       dmax = max(dmax, found ? dg[k] : 0u);
     }
     constexpr int kFirst = 2;
-#endif
     if (foundm && level_out) {
 #pragma unroll
       for (int k = 0; k < KB; ++k)
@@ -1588,19 +1544,14 @@ __global__ void make_vinfo(const int64_t* rs, const int32_t* col, int64_t n, VIn
   }
 }
 
-// hot[v] (RB_HOT1): {first neighbour of v in bottom-up scan order (-1 if
-// none), degree}; else the first two neighbours (-1 if absent)
+// hot[v] = the first two neighbours of v in bottom-up scan order (-1 if absent)
 __global__ void make_hot(const int64_t* rs, const int32_t* col, int64_t n, int reverse, int2* hot) {
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s = rs[v], e = rs[v + 1];
     const int64_t d = e - s;
     int2 h = make_int2(-1, -1);
     if (d > 0) h.x = reverse ? col[e - 1] : col[s];
-#if RB_HOT1
-    h.y = (int32_t)d;
-#else
     if (d > 1) h.y = reverse ? col[e - 2] : col[s + 1];
-#endif
     hot[v] = h;
   }
 }
