@@ -71,7 +71,10 @@ constexpr uint32_t kChunk = 32 * kChunkPerLane;  // edges per hub work item
 constexpr unsigned long long kSliceMask = (1ull << 40) - 1;  // hq_count: rows << 40 | slices
 constexpr int kTdUnroll = 4;                     // light batch: edges per lane per step
 constexpr int kUB = 4;                           // top-down: rows per lane per round
-constexpr int64_t kDenseFrontier = 8192;         // top-down: word-granular dealing from this frontier size
+#ifndef RB_DENSE_NF
+#define RB_DENSE_NF 1024  // measured: 256 / 1024 / 8192 -> s22 95.8 / 95.9 / 96.7 us, s26 433 / 433 / 434
+#endif
+constexpr int64_t kDenseFrontier = RB_DENSE_NF;         // top-down: word-granular dealing from this frontier size
 constexpr int kBU = 8;                           // bottom-up: max words per warp step (template KB <= kBU)
 constexpr int64_t kSmallGraph = 1ll << 23;       // n_dev up to this: 4-word bottom-up steps (shorter chains)
 constexpr int kList = 256;                       // top-down: rows per warp list round
