@@ -74,7 +74,8 @@ constexpr int kUB = 4;                           // top-down: rows per lane per 
 #ifndef RB_DENSE_NF
 #define RB_DENSE_NF 1024  // measured: 256 / 1024 / 8192 -> s22 95.8 / 95.9 / 96.7 us, s26 433 / 433 / 434
 #endif
-constexpr int64_t kDenseFrontier = RB_DENSE_NF;         // top-down: word-granular dealing from this frontier size
+constexpr int64_t kDenseFrontier = RB_DENSE_NF;
+constexpr int64_t kLightToB = 1024;              // top-down: small hub levels claim light rows in phase B         // top-down: word-granular dealing from this frontier size
 constexpr int kBU = 8;                           // bottom-up: max words per warp step (template KB <= kBU)
 constexpr int64_t kSmallGraph = 1ll << 23;       // n_dev up to this: 4-word bottom-up steps (shorter chains)
 constexpr int kList = 256;                       // top-down: rows per warp list round
@@ -238,6 +239,7 @@ struct TdCtx {
   uint8_t* nznext;
   bool probe;  // probe visited bits before the atomic (most targets visited)
   bool defer;  // fire-and-forget claims; the next frontier is counted after the level (count_next)
+  uint32_t hub_min;  // rows longer than this go to phase B (kLightDeg; kTinyDeg on small hub levels)
 };
 
 __device__ __forceinline__ QEnt ld_qent(const QEnt* q) {
@@ -441,7 +443,7 @@ __device__ __forceinline__ void td_list(const TdCtx& c, const uint32_t* lst, uin
         tw[2 * k + 1] = n1[k];
         ta[2 * k] = tiny;
         ta[2 * k + 1] = tiny && d[k] == 2;
-        hub[k] = on[k] && d[k] > kLightDeg;
+        hub[k] = on[k] && d[k] > c.hub_min;
         if (on[k] && !hub[k]) acc.scan += d[k];
       }
       td_claim<2 * kUB>(c, tv, tw, ta, acc);
@@ -450,7 +452,7 @@ __device__ __forceinline__ void td_list(const TdCtx& c, const uint32_t* lst, uin
     uint32_t ld[kUB], lsum = 0;
 #pragma unroll
     for (int k = 0; k < kUB; ++k) {
-      ld[k] = (on[k] && d[k] > kTinyDeg && d[k] <= kLightDeg) ? d[k] : 0u;
+      ld[k] = (on[k] && d[k] > kTinyDeg && d[k] <= c.hub_min) ? d[k] : 0u;
       lsum += ld[k];
     }
     const uint32_t li = rb::warp_incl_scan(lsum);
@@ -1380,6 +1382,9 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
       // many neighbours (RB_PROBE_MF: from this many frontier edges)
       c.probe = 2 * mu < p.m_directed || mf >= p.probe_mf;
       c.defer = mf >= p.defer_mf;
+      // a small frontier with hub rows: its light rows join phase B too, so
+      // phase A (which ends at a grid barrier) is only find rows + publish
+      c.hub_min = (hubs && nf <= kLightToB) ? kTinyDeg : kLightDeg;
       if (c.defer) {  // snapshot of vis at the level start (see count_next)
         for (uint64_t i = gtid; i < (uint64_t)p.n_words / 4; i += gthreads)
           reinterpret_cast<uint4*>(fnext)[i] = __ldcg(reinterpret_cast<const uint4*>(p.vis) + i);
