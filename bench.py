@@ -49,6 +49,10 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-roots", type=int, default=0, help="only run N roots (for ncu)")
+    ap.add_argument("--partitioned", action="store_true",
+                    help="N > 1: ONE traversal per root over the 1D vertex-block partition (NCCL exchange per "
+                         "level; for graphs beyond one GPU).  Default: the 64 independent roots are sharded "
+                         "over the GPUs, each with its own replica of the graph (no data-path collective)")
     ap.add_argument("--validate-roots", type=int, default=64,
                     help="validate this many of the timed roots' trees on the GPU (outside the timed region)")
     a = ap.parse_args()
@@ -92,7 +96,7 @@ def level_bytes(levels, n_dev: int, n_plus_dev: int):
         else:
             U = max(n_plus_dev - reached, 0)
             b = 3 * (n_dev // 8) + 8 * U + 4 * r.scanned_edges + n_next * 4
-        out.append((d, int(b), float(r.wall_time)))
+        out.append((d, int(b), float(getattr(r, "wall_time", 0.0))))
     return out
 
 
@@ -350,7 +354,7 @@ def run_ours(args):
     raw = np.array(raw, np.int64)
     del lab, el
 
-    if world > 1:
+    if world > 1 and args.partitioned:
         return run_partitioned(args, rb, torch, dist, g2, stats, roots, raw, world, rank,
                                {"generate": t_gen, "csr_build": t_csr, "rcm_plus_relabel": t_rcm})
     eng = rb.BfsEngine(g2, rb.BfsParams(mode=args.mode))
