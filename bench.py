@@ -397,7 +397,7 @@ def run_ours(args):
     e2e_teps = []
     for j in my[:3]:  # warm the host path (pinned staging buffers, result-array pool of the allocator)
         eng.run(int(roots[j]))
-    for j in my[: min(len(my), 32)]:
+    for j in my:  # every timed root (the hmean is sensitive to host-side outliers)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         res = eng.run(int(roots[j]))
