@@ -585,34 +585,41 @@ RB_LEVEL_FN void td_rows_items(const TdCtx& c, const uint8_t* nzcur, QEnt* hq, u
 // End of a deferred top-down level: fnext (holding vis as it was at the
 // level start) becomes the next frontier vis & ~fnext, with its nonzero
 // summary; counters n_next = popcount, deg_next = sum of the degrees of the
-// new bits (one coalesced 128-B load of deg[] per nonzero word, 4 words in
-// flight), max degree.  Streaming passes instead of per-claim random traffic.
+// new bits, max degree.  Streaming passes instead of per-claim random traffic.
 __device__ void count_next(const KParams& p, uint32_t* fnext, uint8_t* nznext, Acc& acc) {
+  // Lane l owns word w0 + l: its next-frontier bits, and -- if any -- the 32
+  // degrees of that word as eight 16-B loads, all in flight together (one
+  // round trip per 32 words instead of one per 4 nonzero words).
   const uint32_t lane = rb::lane_id();
   const uint64_t nw = (uint64_t)p.n_words;
   const uint64_t stride = (uint64_t)gridDim.x * kWarps * 32;
   for (uint64_t w0 = warp_slot() * 32; w0 < nw; w0 += stride) {
-    const uint32_t x = __ldcg(p.vis + w0 + lane) & ~__ldcg(fnext + w0 + lane);
-    fnext[w0 + lane] = x;
-    nznext[w0 + lane] = x != 0u ? 1u : 0u;
+    const uint64_t w = w0 + lane;
+    const uint32_t x = __ldcg(p.vis + w) & ~__ldcg(fnext + w);
+    fnext[w] = x;
+    nznext[w] = x != 0u ? 1u : 0u;
     acc.n += __popc(x);
-    uint32_t m = __ballot_sync(RB_FULL, x != 0u);
-    while (m) {
-      uint32_t d[4];
+    if (!x) continue;
+    if ((int64_t)(w + 1) * 32 <= p.n_dev) {
+      const int4* dp = reinterpret_cast<const int4*>(p.deg + (int64_t)w * 32);
+      int4 q[8];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        d[q] = 0u;
-        if (m) {
-          const uint32_t j = __ffs(m) - 1;
-          m &= m - 1;
-          const uint32_t xj = __shfl_sync(RB_FULL, x, j);  // m is warp-uniform
-          if ((xj >> lane) & 1u) d[q] = (uint32_t)rb::ldg_i32(p.deg + (int64_t)(w0 + j) * 32 + lane);
+      for (int j = 0; j < 8; ++j) q[j] = __ldg(dp + j);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t dv[4] = {(uint32_t)q[j].x, (uint32_t)q[j].y, (uint32_t)q[j].z, (uint32_t)q[j].w};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const uint32_t d = ((x >> (4 * j + c)) & 1u) ? dv[c] : 0u;
+          acc.deg += d;
+          acc.maxdeg = max(acc.maxdeg, d);
         }
       }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        acc.deg += d[q];
-        acc.maxdeg = max(acc.maxdeg, d[q]);
+    } else {  // the word holding the end of the vertex range: no reads past deg[n_dev)
+      for (uint32_t y = x; y; y &= y - 1) {
+        const uint32_t d = (uint32_t)rb::ldg_i32(p.deg + (int64_t)w * 32 + (__ffs(y) - 1));
+        acc.deg += d;
+        acc.maxdeg = max(acc.maxdeg, d);
       }
     }
   }
