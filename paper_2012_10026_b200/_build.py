@@ -57,7 +57,8 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, ex
     if out == LIB and not extra and not force and not _stale():
         return LIB
     nvcc = _nvcc()
-    objdir = os.path.join(PKG, "_obj")
+    # tuning variants keep their objects out of the tree (the repo travels to the GPU box)
+    objdir = os.path.join(PKG, "_obj") if out == LIB else os.path.join("/tmp", "rb_build_obj")
     os.makedirs(objdir, exist_ok=True)
     objs = []
     logs = []
