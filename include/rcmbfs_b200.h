@@ -150,12 +150,18 @@ int rb_bfs_traverse(rb_bfs* h, void* stream);
 int rb_bfs_elapsed(rb_bfs* h, double* seconds);
 /* Copy results; parents/levels cover [0,n_dev); n_records <= cap. */
 /* Asynchronous result path (BfsEngine.run, engine.py:518-604): enqueue the
- * copies of the launch state (rb_bfs_state_bytes() bytes) and of the first
- * `cap` level records behind the traversal on `stream`, without waiting.
+ * copies of the launch state (rb_bfs_state_bytes() bytes), of the first `cap`
+ * level records and (if h_parent) of the parents in `chunks` pieces behind
+ * the traversal on `stream`, without waiting.
  * After the caller synchronizes the stream, rb_bfs_complete() returns 0 and
  * the record count when that launch finished the traversal, or 1 when the
  * caller must drain with rb_bfs_results (continuation launches). */
-int rb_bfs_results_async(rb_bfs* h, void* h_state, rb_level_record* h_records, int64_t cap, void* stream);
+int rb_bfs_results_async(rb_bfs* h, void* h_state, rb_level_record* h_records, int64_t cap, int32_t* h_parent,
+                         int32_t chunks, void* stream);
+/* Wait for those copies: what = -1 the state + records, what = i (< chunks,
+ * <= 8) the i-th of `chunks` equal pieces of the parents [0, n_dev) that were
+ * enqueued into h_parent (pinned host memory). */
+int rb_bfs_wait(rb_bfs* h, int32_t what);
 int rb_bfs_complete(rb_bfs* h, const void* h_state, const rb_level_record* h_records, int64_t cap,
                     int64_t* n_records);
 size_t rb_bfs_state_bytes(void);

@@ -68,7 +68,8 @@ _SIGS = {
     "rb_bfs_traverse": ([P, P], ctypes.c_int),
     "rb_bfs_elapsed": ([P, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
     "rb_bfs_results": ([P, P, P, P, I64, ctypes.POINTER(I64), P], ctypes.c_int),
-    "rb_bfs_results_async": ([P, P, P, I64, P], ctypes.c_int),
+    "rb_bfs_results_async": ([P, P, P, I64, P, I32, P], ctypes.c_int),
+    "rb_bfs_wait": ([P, I32], ctypes.c_int),
     "rb_bfs_complete": ([P, P, P, I64, ctypes.POINTER(I64)], ctypes.c_int),
     "rb_bfs_state_bytes": ([], SZ),
     "rb_bfs_step": ([P, ctypes.c_int, P, P, P, P, P, P, P, P], ctypes.c_int),

@@ -1619,6 +1619,8 @@ __global__ void make_pad_mask(uint32_t* m, int64_t n_dev, int64_t n_words) {
 // ---------------------------------------------------------------------------
 // host side
 
+constexpr int kMaxChunks = 8;  // async result path: parent copy chunks
+
 struct rb_bfs {
   KParams kp;
   rb_bfs_params prm;
@@ -1637,6 +1639,7 @@ struct rb_bfs {
   std::vector<rb_level_record> recs;
   int64_t levels_per_launch;  // kRecCap; RB_LEVELS_PER_LAUNCH=1 gives one launch per level (profiling)
   cudaEvent_t ev_start, ev_end;  // bracket all launches of one traversal
+  cudaEvent_t ev_chunk[kMaxChunks + 1];  // async result path: parent chunks, then the small copies
   bool launched;
   bool solo;      // run the first small levels in one CTA (solo_levels); RB_SOLO=0 disables
   bool exec_opt;  // executed direction by cost; RB_EXEC_OPT=0 disables
@@ -1703,6 +1706,7 @@ extern "C" int rb_bfs_create_part(const int64_t* d_row_starts, const int32_t* d_
   if (const char* env = getenv("RB_BU_SPARSE")) h->kp.bu_sparse = atoll(env);
   cudaEventCreate(&h->ev_start);
   cudaEventCreate(&h->ev_end);
+  for (int i = 0; i <= kMaxChunks; ++i) cudaEventCreateWithFlags(&h->ev_chunk[i], cudaEventDisableTiming);
   if (const char* env = getenv("RB_DEBUG")) h->kp.debug = atoi(env);
   h->kp.dbg = nullptr;
   if (const char* env = getenv("RB_LEVELS_PER_LAUNCH")) {
@@ -1833,6 +1837,8 @@ extern "C" int rb_bfs_destroy(rb_bfs* h) {
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (h->ev_start) cudaEventDestroy(h->ev_start);
+  for (int i = 0; i <= kMaxChunks; ++i)
+    if (h->ev_chunk[i]) cudaEventDestroy(h->ev_chunk[i]);
   if (h->ev_end) cudaEventDestroy(h->ev_end);
   delete h;
   return RB_OK;
@@ -1968,13 +1974,31 @@ extern "C" int rb_bfs_results(rb_bfs* h, int32_t* parent_out, int32_t* level_out
 // single launch finished the traversal (returns 0) -- else it returns 1 and
 // the caller drains with rb_bfs_results (very deep graphs: continuations).
 extern "C" int rb_bfs_results_async(rb_bfs* h, void* h_state, rb_level_record* h_records, int64_t cap,
-                                    void* stream) {
-  if (!h || !h_state || (cap > 0 && !h_records)) return RB_ERR_ARG;
+                                    int32_t* h_parent, int32_t chunks, void* stream) {
+  if (!h || !h_state || (cap > 0 && !h_records) || chunks < 0 || chunks > kMaxChunks) return RB_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
   RB_CUDA_TRY(cudaMemcpyAsync(h_state, h->kp.fin, sizeof(Final), cudaMemcpyDeviceToHost, s));
   if (cap > 0)
     RB_CUDA_TRY(cudaMemcpyAsync(h_records, h->kp.rec, (size_t)(cap < kRecCap ? cap : kRecCap) * sizeof(rb_level_record),
                                 cudaMemcpyDeviceToHost, s));
+  RB_CUDA_TRY(cudaEventRecord(h->ev_chunk[kMaxChunks], s));  // the small copies
+  if (h_parent && chunks > 0) {  // parents [0, n_dev) in `chunks` pieces, an event behind each
+    const int64_t step = (h->n_dev + chunks - 1) / chunks;
+    for (int32_t i = 0; i < chunks; ++i) {
+      const int64_t a = i * step, b = a + step < h->n_dev ? a + step : h->n_dev;
+      if (b > a)
+        RB_CUDA_TRY(cudaMemcpyAsync(h_parent + a, h->kp.parent + a, (size_t)(b - a) * 4, cudaMemcpyDeviceToHost, s));
+      RB_CUDA_TRY(cudaEventRecord(h->ev_chunk[i], s));
+    }
+  }
+  return RB_OK;
+}
+
+// Wait for the async result copies: what = -1 the launch state + records,
+// what = i the parent chunk i.
+extern "C" int rb_bfs_wait(rb_bfs* h, int32_t what) {
+  if (!h || what < -1 || what >= kMaxChunks) return RB_ERR_ARG;
+  RB_CUDA_TRY(cudaEventSynchronize(h->ev_chunk[what < 0 ? kMaxChunks : what]));
   return RB_OK;
 }
 

@@ -298,35 +298,27 @@ class _DeviceBfs:
         if self._state is None:
             self._state = torch.empty(int(L.rb_bfs_state_bytes()) // 8, dtype=torch.int64, pin_memory=True)
             self._recs_pin = torch.empty(_REC_FAST * 10, dtype=torch.int64, pin_memory=True)
-        _lib.check(L.rb_bfs_results_async(self.h, _lib.ptr(self._state), _lib.ptr(self._recs_pin), _REC_FAST, s),
-                   "rb_bfs_results_async")
-        ev_small = torch.cuda.Event()
-        ev_small.record()
         n_dev = self.n_dev
-        dev = _ptr_view(L.rb_bfs_parent_ptr(self.h), n_dev)
         chunks = chunks or (4 if n_dev >= (8 << 20) else 2)
-        step = -(-n_dev // chunks)
-        evs = []
-        for a in range(0, n_dev, step):
-            b = min(a + step, n_dev)
-            self.pinned[a:b].copy_(dev[a:b], non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record()
-            evs.append((a, b, ev))
+        _lib.check(L.rb_bfs_results_async(self.h, _lib.ptr(self._state), _lib.ptr(self._recs_pin), _REC_FAST,
+                                          _lib.ptr(self.pinned), chunks, s), "rb_bfs_results_async")
         pred = fresh_int32(n)
         pt = torch.from_numpy(pred)
         if n > n_dev:
             pt[n_dev:].fill_(-1)
-        ev_small.synchronize()
+        _lib.check(L.rb_bfs_wait(self.h, -1), "rb_bfs_wait")
         nrec = ctypes.c_int64(0)
         done = L.rb_bfs_complete(self.h, _lib.ptr(self._state), _lib.ptr(self._recs_pin), _REC_FAST,
                                  ctypes.byref(nrec))
         if done == 0:
             recs = (_lib.LevelRecordC * nrec.value).from_buffer_copy(
                 self._recs_pin.numpy().tobytes()[: nrec.value * ctypes.sizeof(_lib.LevelRecordC)])
-            for a, b, ev in evs:
-                ev.synchronize()
-                pt[a:b].copy_(self.pinned[a:b])
+            step = -(-n_dev // chunks)
+            for i in range(chunks):
+                a, b = i * step, min((i + 1) * step, n_dev)
+                _lib.check(L.rb_bfs_wait(self.h, i), "rb_bfs_wait")
+                if b > a:
+                    pt[a:b].copy_(self.pinned[a:b])
             el = ctypes.c_double(0.0)
             _lib.check(L.rb_bfs_elapsed(self.h, ctypes.byref(el)), "rb_bfs_elapsed")
             return pred, recs, el.value

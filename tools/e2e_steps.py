@@ -24,15 +24,14 @@ for r in roots[:16]:
     L = _lib.lib(); s = _lib.stream_ptr()
     t = time.perf_counter()
     d.traverse(int(r)); t = tick("traverse", t)
-    _lib.check(L.rb_bfs_results_async(d.h, _lib.ptr(d._state), _lib.ptr(d._recs_pin), 64, s)); ev = torch.cuda.Event(); ev.record(); t = tick("enqueue small", t)
-    dev = engine._ptr_view(L.rb_bfs_parent_ptr(d.h), d.n_dev); step = -(-d.n_dev // 4); evs = []
-    for a in range(0, d.n_dev, step):
-        b = min(a + step, d.n_dev); d.pinned[a:b].copy_(dev[a:b], non_blocking=True); e = torch.cuda.Event(); e.record(); evs.append((a, b, e))
-    t = tick("enqueue chunks", t)
-    pred = engine.fresh_int32(g2.n); pt = torch.from_numpy(pred); pt[d.n_dev:].fill_(-1); t = tick("alloc+tail", t)
-    ev.synchronize(); t = tick("wait small", t)
+    n_dev = d.n_dev; chunks = 4 if n_dev >= (8 << 20) else 2
+    _lib.check(L.rb_bfs_results_async(d.h, _lib.ptr(d._state), _lib.ptr(d._recs_pin), 64, _lib.ptr(d.pinned), chunks, s)); t = tick("enqueue copies", t)
+    pred = engine.fresh_int32(g2.n); pt = torch.from_numpy(pred); pt[n_dev:].fill_(-1); t = tick("alloc+tail", t)
+    L.rb_bfs_wait(d.h, -1); t = tick("wait small", t)
     nrec = ctypes.c_int64(0); L.rb_bfs_complete(d.h, _lib.ptr(d._state), _lib.ptr(d._recs_pin), 64, ctypes.byref(nrec)); t = tick("complete", t)
-    for a, b, e in evs: e.synchronize(); pt[a:b].copy_(d.pinned[a:b])
+    step = -(-n_dev // chunks)
+    for i in range(chunks):
+        a, b = i * step, min((i + 1) * step, n_dev); L.rb_bfs_wait(d.h, i); pt[a:b].copy_(d.pinned[a:b])
     t = tick("chunks", t)
     lv = engine._records_to_levels((_lib.LevelRecordC * nrec.value).from_buffer_copy(d._recs_pin.numpy().tobytes()[: nrec.value * 80])); t = tick("records->levels", t)
 print(f"n={g2.n} n_dev={d.n_dev}")
