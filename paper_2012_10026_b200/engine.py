@@ -299,7 +299,8 @@ class _DeviceBfs:
             self._state = torch.empty(int(L.rb_bfs_state_bytes()) // 8, dtype=torch.int64, pin_memory=True)
             self._recs_pin = torch.empty(_REC_FAST * 10, dtype=torch.int64, pin_memory=True)
         n_dev = self.n_dev
-        chunks = chunks or (4 if n_dev >= (8 << 20) else 2)
+        # 8 pieces (the ABI maximum): measured best at s22 and s26 (1 / 2 / 4 / 8 -> 128 / 146 / 156 / 159 e2e GTEPS at s22)
+        chunks = chunks or int(os.environ.get("RB_E2E_CHUNKS", "0")) or 8
         _lib.check(L.rb_bfs_results_async(self.h, _lib.ptr(self._state), _lib.ptr(self._recs_pin), _REC_FAST,
                                           _lib.ptr(self.pinned), chunks, s), "rb_bfs_results_async")
         pred = fresh_int32(n)
