@@ -159,7 +159,7 @@ int rb_bfs_elapsed(rb_bfs* h, double* seconds);
 int rb_bfs_results_async(rb_bfs* h, void* h_state, rb_level_record* h_records, int64_t cap, int32_t* h_parent,
                          int32_t chunks, void* stream);
 /* Wait for those copies: what = -1 the state + records, what = i (< chunks,
- * <= 8) the i-th of `chunks` equal pieces of the parents [0, n_dev) that were
+ * <= 32) the i-th of `chunks` equal pieces of the parents [0, n_dev) that were
  * enqueued into h_parent (pinned host memory). */
 int rb_bfs_wait(rb_bfs* h, int32_t what);
 int rb_bfs_complete(rb_bfs* h, const void* h_state, const rb_level_record* h_records, int64_t cap,

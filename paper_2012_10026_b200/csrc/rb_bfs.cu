@@ -1619,7 +1619,7 @@ __global__ void make_pad_mask(uint32_t* m, int64_t n_dev, int64_t n_words) {
 // ---------------------------------------------------------------------------
 // host side
 
-constexpr int kMaxChunks = 8;  // async result path: parent copy chunks
+constexpr int kMaxChunks = 32;  // async result path: parent copy chunks
 
 struct rb_bfs {
   KParams kp;
