@@ -190,6 +190,7 @@ struct KParams {
   int64_t td_m;           // entries of td_col
   int64_t exec_alpha;     // early levels labelled bottom-up run top-down if m_f * exec_alpha <= m_u
   int64_t bu_sparse;      // late bottom-up levels with few unvisited vertices run over a list
+  uint32_t* solo_q;       // the frontier the solo start levels hand to the grid (kSoloCap entries)
   uint32_t* ul0;          // unvisited-vertex lists (alternating by level parity)
   uint32_t* ul1;
   int64_t src;
@@ -537,6 +538,21 @@ RB_LEVEL_FN void td_rows_words(const TdCtx& c, QEnt* hq, uint32_t* hs, unsigned 
       __syncwarp();
       td_list(c, lst, tot, hq, hs, hq_count, acc);
     }
+  }
+}
+
+// Top-down phase A from a frontier list (the one the solo levels leave):
+// warp slot s takes entries [32 s, 32 s + 32).
+__device__ void td_rows_list(const TdCtx& c, const uint32_t* q, uint32_t n, QEnt* hq, uint32_t* hs,
+                             unsigned long long* hq_count, Acc& acc, uint32_t* lst) {
+  const uint32_t lane = rb::lane_id();
+  const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
+  for (uint64_t b = warp_slot() * 32; b < n; b += nwarps * 32) {
+    const uint32_t tot = (uint32_t)min((uint64_t)32, n - b);
+    __syncwarp();
+    if (lane < tot) lst[lane] = __ldcg(q + b + lane);
+    __syncwarp();
+    td_list(c, lst, tot, hq, hs, hq_count, acc);
   }
 }
 
@@ -1228,7 +1244,12 @@ __device__ __forceinline__ void solo_levels(const KParams& p, uint32_t* smem, So
     ++L;
     ++done;
     __syncthreads();  // everyone has read sh before the next level resets it
-    if (!(nf > 0 && dir == 0 && nf <= kSoloCap && mf <= kSoloMf && done < p.max_levels)) break;
+    if (!(nf > 0 && dir == 0 && nf <= kSoloCap && mf <= kSoloMf && done < p.max_levels)) {
+      // hand the next frontier to the grid as a list (its first level then
+      // skips the summary walk): complete when it fits the shared buffer
+      for (int64_t i = tid; i < nf && nf <= kSoloCap; i += kThreads) p.solo_q[i] = qn[i];
+      break;
+    }
     uint32_t* t = qp;
     qp = qc;
     qc = qn;
@@ -1275,6 +1296,9 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
   int64_t reached = p.reached0;
   uint32_t epoch = 0;
   bool solo_hubs = false;
+  __shared__ unsigned long long s_fin[9];  // the state after the solo levels ([8]: frontier list length)
+  if (threadIdx.x == 0) s_fin[0] = ~0ull, s_fin[8] = 0ull;
+  __syncthreads();
   if (p.from_fin && mf <= kSoloMf) {
     // traversal start with a small frontier: CTA 0 runs the first levels
     // alone, the grid waits at one barrier and picks up the state
@@ -1292,18 +1316,19 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
         p.fin->mf = mf;
         p.fin->mu = mu;
         p.fin->pad = h ? 1 : 0;
+        p.fin->pad2 = (nf > 0 && nf <= kSoloCap) ? nf : 0;  // p.solo_q holds the frontier
       }
     }
     {
       // the state after the solo levels: thread 0 of each CTA fetches it
       // into shared memory (all threads loading it would queue on one line)
-      const unsigned long long* const src[8] = {
+      const unsigned long long* const src[9] = {
           (const unsigned long long*)&p.fin->levels_done, (const unsigned long long*)&p.fin->L,
           (const unsigned long long*)&p.fin->dir,         (const unsigned long long*)&p.fin->nf,
           (const unsigned long long*)&p.fin->mf,          (const unsigned long long*)&p.fin->mu,
-          (const unsigned long long*)&p.fin->pad,         (const unsigned long long*)&p.fin->reached};
-      __shared__ unsigned long long s_fin[8];
-      rb::grid_barrier_fetch<8>(p.bar, nblocks, epoch, src, s_fin);
+          (const unsigned long long*)&p.fin->pad,         (const unsigned long long*)&p.fin->reached,
+          (const unsigned long long*)&p.fin->pad2};
+      rb::grid_barrier_fetch<9>(p.bar, nblocks, epoch, src, s_fin);
       done = (int64_t)s_fin[0];
       L = (int64_t)s_fin[1];
       dir = (int)s_fin[2];
@@ -1399,7 +1424,9 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
         if (p.dbg && blockIdx.x == 0 && threadIdx.x == 0 && done < 64) p.dbg[kDbgPhase + done * 8 + 0] = globaltimer();
       }
       // phase A: frontier rows from the bitmap; hub rows become slices in hq
-      if (nf >= kDenseFrontier)
+      if (s_fin[8] && done == (int64_t)s_fin[0])  // the first grid level after the solo levels
+        td_rows_list(c, p.solo_q, (uint32_t)s_fin[8], hq, hs, &in->hq_count, acc, s_bu_pair[threadIdx.x >> 5]);
+      else if (nf >= kDenseFrontier)
         td_rows_words(c, hq, hs, &in->hq_count, acc, s_bu_pair[threadIdx.x >> 5], &s_bu_next[L & 1]);
       else
         td_rows_items(c, p.nzcur_ext ? p.nzcur_ext : nz_of(p, r0), hq, hs, &in->hq_count, acc,
@@ -1740,6 +1767,7 @@ extern "C" int rb_bfs_create_part(const int64_t* d_row_starts, const int32_t* d_
   RB_ALLOC(k.hq1, nhub * sizeof(QEnt));
   RB_ALLOC(k.hs0, nhub * sizeof(uint32_t));
   RB_ALLOC(k.hs1, nhub * sizeof(uint32_t));
+  RB_ALLOC(k.solo_q, kSoloCap * sizeof(uint32_t));
   RB_ALLOC(k.ul0, ((size_t)n_dev / kListRatio + 1024) * sizeof(uint32_t));
   RB_ALLOC(k.ul1, ((size_t)n_dev / kListRatio + 1024) * sizeof(uint32_t));
 
@@ -1832,7 +1860,7 @@ extern "C" int rb_bfs_create_part(const int64_t* d_row_starts, const int32_t* d_
 extern "C" int rb_bfs_destroy(rb_bfs* h) {
   if (!h) return RB_OK;
   KParams& k = h->kp;
-  void* ptrs[] = {k.vis, k.fb0, k.fb1, k.fb2, h->vis_template, h->pad_mask, k.hq0, k.hq1, k.hs0, k.hs1, k.ul0, k.ul1, k.parent,
+  void* ptrs[] = {k.vis, k.fb0, k.fb1, k.fb2, h->vis_template, h->pad_mask, k.hq0, k.hq1, k.hs0, k.hs1, k.ul0, k.ul1, k.solo_q, k.parent,
                   k.level, k.slots, k.bar, k.rec, k.fin, k.nz0, k.nz1, k.nz2, h->hot, h->vinfo, k.dbg, h->td_vinfo};
   for (void* q : ptrs)
     if (q) cudaFree(q);
