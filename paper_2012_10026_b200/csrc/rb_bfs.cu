@@ -59,6 +59,9 @@ namespace {
 #define RB_THREADS 768  // 24 warps x 80 registers: measured best (1024 x 64 spills in the bottom-up loop; s22 -8%, s26 -6%, Chung-Lu -9%)
 #endif
 constexpr int kThreads = RB_THREADS;
+#ifndef RB_BU_DEFER_CONT
+#define RB_BU_DEFER_CONT 1  // bottom-up: continuation rows queued per warp and run 32 at a time
+#endif
 #define RB_LEVEL_FN __device__  // (tried __noinline__ level bodies: call-ABI spills, s26 +35%)
 #ifndef RB_MINB
 #define RB_MINB 1
@@ -785,6 +788,69 @@ RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uin
     k = __shfl_sync(RB_FULL, k, 0);
     return ((uint64_t)blockIdx.x + (uint64_t)k * gridDim.x) * KB;
   };
+#if RB_BU_DEFER_CONT
+  // Deferred continuation: rows that miss both hot checks are queued per warp
+  // (s_pair, global vertex ids) and continued 32 at a time, one per lane, so a
+  // step's round 1 does not wait on a few rows' dependent row-start / column
+  // loads and continuation batches run with every lane busy.  Found vertices
+  // set their (already written) words with reds.
+  uint32_t npend = 0;
+  auto continue_batch = [&](uint32_t nb, const uint32_t* q) {
+    const bool mine = lane < nb;
+    int64_t v = 0, s0 = 0;
+    uint32_t d = 0;
+    int32_t par = -1;
+    uint32_t chk = 0;
+    if (mine) {
+      v = (int64_t)q[lane];
+      d = (uint32_t)rb::ldg_i32(p.deg + v);
+      s0 = rb::ldg_i64(p.rs + v);
+      const int64_t e0 = s0 + d;
+      const int64_t lim = d < (uint32_t)kK2 ? d : kK2;
+      for (int64_t t0 = 2; par < 0 && t0 < lim; t0 += 8) {
+        int32_t uu[8];
+        uint32_t bb[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+          uu[t] = (t0 + t < lim) ? rb::ldg_i32(p.col_bu + bu_idx<kRev>(s0, e0, t0 + t)) : -1;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) bb[t] = uu[t] >= 0 ? ld_bits(fcur + (uu[t] >> 5)) : 0u;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          if (par < 0 && uu[t] >= 0) {
+            ++chk;
+            if ((bb[t] >> (uu[t] & 31)) & 1u) par = uu[t];
+          }
+        }
+      }
+    }
+    uint32_t hm = __ballot_sync(RB_FULL, mine && par < 0 && d > (uint32_t)kK2);
+    while (hm) {
+      const int h = __ffs(hm) - 1;
+      hm &= hm - 1;
+      const int64_t hs = rb::shfl_i64(s0, h);
+      const int64_t he = hs + __shfl_sync(RB_FULL, d, h);
+      int64_t hc = 0;
+      const int32_t hp = bu_heavy<kRev>(p, fcur, hs, he, kK2, &hc);
+      if ((int)lane == h) {
+        chk += (uint32_t)hc;
+        par = hp;
+      }
+    }
+    acc.scan += chk;
+    if (mine && par >= 0) {
+      const uint32_t bit = 1u << (v & 31);
+      p.parent[v] = par;
+      if (p.level) p.level[v] = (int32_t)(L + 1);
+      red_or(fnext + (v >> 5), bit);
+      red_or(p.vis + (v >> 5), bit);
+      nznext[v >> 5] = 1u;
+      acc.n += 1;
+      acc.deg += d;
+      acc.maxdeg = max(acc.maxdeg, d);
+    }
+  };
+#endif
   uint64_t w_nx = claim_step();
   uint32_t vw_nx = (w_nx < nw && lane < KB) ? __ldcg(p.vis + w_nx + lane) : 0xffffffffu;
   while (w_nx < nw) {
@@ -856,6 +922,35 @@ RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uin
     const uint32_t np = __popc(needm);
     const uint32_t incl = rb::warp_incl_scan(np);
     const uint32_t npairs = __shfl_sync(RB_FULL, incl, 31);
+#if RB_BU_DEFER_CONT
+    if (!kCollect) {
+      if (npairs) {  // queue the rows (global ids) behind the pending ones
+        uint32_t pos = npend + incl - np;
+        for (uint32_t m = needm; m; m &= m - 1) {
+          const uint32_t k = __ffs(m) - 1;
+          s_pair[pos++] = (uint32_t)((w0 + k) * 32 + lane);
+        }
+        npend += npairs;
+      }
+      __syncwarp();
+      if (lane < (uint32_t)KB) {  // round-1 results: the warp owns these words
+        const uint32_t fm = fm_s[lane];
+        if (fm) {
+          fnext[w0 + lane] = fm;
+          nznext[w0 + lane] = 1u;
+          p.vis[w0 + lane] = vw | fm;
+        }
+      }
+      __syncwarp();
+      while (npend >= 32) {  // full batches from the top of the queue
+        npend -= 32;
+        continue_batch(32, s_pair + npend);
+        __syncwarp();
+      }
+      acc.scan += checks;
+      continue;
+    }
+#endif
     if (npairs) {
       uint32_t pos = incl - np;
       for (uint32_t m = needm; m; m &= m - 1) {
@@ -946,6 +1041,9 @@ RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uin
     __syncwarp();
     acc.scan += checks;
   }
+#if RB_BU_DEFER_CONT
+  if (!kCollect && npend) continue_batch(npend, s_pair);
+#endif
 }
 
 // Sparse bottom-up (late levels, at most one unvisited vertex in 256): the
@@ -1268,7 +1366,7 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
   __shared__ unsigned long long s_red[kWarps * 4];
   __shared__ unsigned long long s_ctr[5];  // [4]: the unvisited list of the last level (bit 40: valid | count)
   __shared__ uint32_t s_bu_found[kWarps][kBU];
-  __shared__ uint32_t s_bu_pair[kWarps][32 * kBU > kList ? 32 * kBU : kList];
+  __shared__ uint32_t s_bu_pair[kWarps][32 * kBU + 32 > kList ? 32 * kBU + 32 : kList];
   __shared__ uint32_t s_bu_next[2];  // bottom-up: next step of this CTA (level parity)
   __shared__ SoloShared s_solo;
   __shared__ uint32_t s_wtot[32];
