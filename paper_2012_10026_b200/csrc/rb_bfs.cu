@@ -17,34 +17,44 @@
 //                plain byte stores, no atomics)
 //   hq[2], hs[2] hub rows {row start, vertex, degree} and the first index of
 //                their 256-edge slices (phase B deals slices over all warps)
-//   vinfo[]      32-B row record {row start, degree, first two neighbours}
+//   vinfo[]      16-B row record {40-bit row start, degree, first two neighbours}
 //   hot[]        int2 per vertex: the first two neighbours in bottom-up order
 //   parent[]     int32; level[] only when the caller asks for it
+//   ul[2]        sparse bottom-up: the vertices still unvisited (tail levels)
+//   solo_q       the frontier the solo start levels hand to the grid
 // Invariant: vis holds every vertex discovered so far (the current frontier
 // included), so a top-down claim is one atomicOr on vis and a bottom-up step
 // tests ~vis directly.
 //
 // The path is latency-bound integer work, so both directions are written for
 // memory-level parallelism: every lane keeps several independent loads in
-// flight, work items are dealt statically so the whole grid is busy, and
-// there is no per-item atomic work fetching.
+// flight and work is dealt so that the whole grid is busy.
 //
-// Top-down (phase A, td_rows): warps walk the nonzero summary of the frontier
-// bitmap; each nonzero 256-vertex item is compacted into a per-warp
-// shared-memory list and its rows' records are loaded 4 per lane.  Rows of
-// degree <= 2 claim the neighbours held in the record, rows of degree <= 32
-// are edge-balanced across the warp, longer rows are appended as 256-edge
-// slices that every warp shares after a grid barrier (phase B, td_hubs).  A
-// neighbour is claimed with one atomicOr on its visited word; the winner sets
-// the next-frontier bit, the nonzero-summary bit and the parent.
-// Bottom-up (bu_level): a warp owns kBU = 8 consecutive bitmap words (256
-// vertices), lane l bit l of each, so visited / next-frontier words are
-// written with plain stores.  Round 1 checks the two scan-first neighbours
+// Levels: CTA 0 runs the first small top-down levels alone (solo_levels,
+// frontier in shared memory, no grid barrier).  Every level keeps the
+// reference policy's direction label but executes the cheaper way (early
+// crossover m_f <= m_u / 11, a latency cost model late).
+// Top-down, phase A (td_rows_*): frontier rows from a list (after the solo
+// levels), from bitmap words dealt over all warps (dense frontiers) or from
+// the nonzero summary (sparse ones); row records are loaded 4 per lane.  Rows
+// of degree <= 2 claim the neighbours held in the record, rows of degree <= 32
+// are edge-balanced across the warp, longer rows are published as hub rows
+// (one entry each) whose 256-edge slices every warp shares after a grid
+// barrier (phase B, td_hubs: a contiguous slice range per warp, columns of
+// the next slice in flight).  A claim is one atomicOr on the visited word
+// (probe first on late or big levels); the winner sets the next-frontier bit,
+// the summary byte and the parent.  Levels with >= 2^20 frontier edges are
+// deferred: racing parent stores + fire-and-forget visited reds, the next
+// frontier and its counters computed afterwards (count_next).
+// Bottom-up (bu_level): a warp owns KB consecutive bitmap words (4 up to 2^23
+// vertices, else 8), lane l bit l of each, so visited / next-frontier words
+// are written with plain stores.  Round 1 checks the two scan-first neighbours
 // from hot[] (reverse row order by default: RCM ids ascend with degree, so
 // the end of a row holds the likely frontier hubs); rows still open are
-// compacted across the warp and continued 8 neighbours per lane per step up
-// to kK2 checks; longer rows are finished by the whole warp 256 neighbours
-// per step with a ballot early exit.
+// queued per warp and continued 32 at a time, 8 neighbours per lane per step
+// up to kK2 checks; longer rows are finished by the whole warp 256 neighbours
+// per step with a ballot early exit.  Late levels of large graphs with few
+// unvisited vertices run over a list of them (bu_sparse_pass).
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
