@@ -56,9 +56,11 @@ for L in sorted(agg):
     rs = agg[L]
     mix = collections.Counter(r.direction[0].upper() + ((r.executed_direction or r.direction)[0].upper()) for r in rs)
     t = np.array([r.wall_time for r in rs]) * 1e6
+    imax = int(np.argmax(t))
     print(f"  L{L:<2d} n={len(rs):2d} {dict(mix)}  t mean {t.mean():7.1f} max {t.max():7.1f} us | "
           f"n_f {np.mean([r.n_f for r in rs]):11.0f} m_f {np.mean([r.m_f for r in rs]):12.0f} "
-          f"scanned {np.mean([r.scanned_edges for r in rs]):11.0f}  sum/64 {t.sum() / len(tot):6.1f}")
+          f"scanned {np.mean([r.scanned_edges for r in rs]):11.0f}  sum/64 {t.sum() / len(tot):6.1f}"
+          f"  | max: n_f {rs[imax].n_f} m_f {rs[imax].m_f}")
     for k in sorted(mix):
         sel = [r for r in rs if r.direction[0].upper() + ((r.executed_direction or r.direction)[0].upper()) == k]
         tk = [r.wall_time * 1e6 for r in sel]
