@@ -69,6 +69,9 @@ namespace {
 #define RB_THREADS 768  // 24 warps x 80 registers: measured best (1024 x 64 spills in the bottom-up loop; s22 -8%, s26 -6%, Chung-Lu -9%)
 #endif
 constexpr int kThreads = RB_THREADS;
+#ifndef RB_SPARSE_ALL
+#define RB_SPARSE_ALL 0  // sparse bottom-up also in the small-graph (4-word step) build
+#endif
 #ifndef RB_BU_DEFER_CONT
 #define RB_BU_DEFER_CONT 1  // bottom-up: continuation rows queued per warp and run 32 at a time
 #endif
@@ -1372,7 +1375,7 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
   // Sparse bottom-up lists only in the large-graph build (8-word steps): at
   // scale 22 the tail levels are latency floors either way and the extra
   // code costs the small-graph kernel ~2% (measured).
-  constexpr bool kSparseOK = KB == 8;
+  constexpr bool kSparseOK = RB_SPARSE_ALL || KB == 8;
   __shared__ unsigned long long s_red[kWarps * 4];
   __shared__ unsigned long long s_ctr[5];  // [4]: the unvisited list of the last level (bit 40: valid | count)
   __shared__ uint32_t s_bu_found[kWarps][kBU];
