@@ -106,7 +106,7 @@ constexpr int64_t kBuVertPs = 5;        // per unvisited vertex
 constexpr int64_t kBuCheckPs = 1;       // per neighbour check (bounded by 8 per unvisited vertex)
 constexpr int64_t kBuSparsePs = 2000000; // sparse bottom-up: the list pass (+ collection barrier)
 constexpr int64_t kSparseRatio = 256;   // sparse bottom-up when at most one vertex in 256 is unvisited
-constexpr int64_t kListRatio = 64;      // a bitmap bottom-up level lists its survivors from one in 64 (list capacity)
+constexpr int64_t kListRatio = 16;      // a bitmap bottom-up level lists its survivors from one in 16 (list capacity)
 constexpr int kK2 = 258;                         // bottom-up: per-lane checks before the warp takes over
 constexpr int kHeavyPerLane = 8;                 // warp-cooperative bottom-up: neighbours per lane per step
 constexpr uint64_t kDbgWarpBase = 65536;  // RB_DEBUG_TS buffer: per-block stamps, then per-warp stamps
