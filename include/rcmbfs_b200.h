@@ -79,15 +79,15 @@ typedef struct rb_bfs rb_bfs;
 
 typedef struct {
   int64_t level;
-  int64_t direction; /* 0 = top_down, 1 = bottom_up */
+  int64_t direction; /* 0 = top_down, 1 = bottom_up (the reference policy's label) */
   int64_t n_f;
   int64_t m_f;
   int64_t m_u;
   int64_t scanned_edges; /* TD: edges examined; BU: neighbour checks */
   int64_t t_ns;          /* device %globaltimer duration of the level */
   int64_t n_next;
-  int64_t t_queue_ns;    /* part of t_ns spent rebuilding the top-down queues */
-  int64_t reserved;
+  int64_t t_queue_ns;    /* part of t_ns before the top-down hub phase (phase A) */
+  int64_t reserved;      /* executed direction: 0 = top_down, 1 = bottom_up */
 } rb_level_record;
 
 typedef struct {
