@@ -45,18 +45,25 @@ def lib():
             build()
         L = ctypes.CDLL(_LIB_PATH)
         P, I64, I32, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
-        L.or_build_csr.argtypes = [I64, I64, P, P, P, P, P]
-        L.or_build_csr.restype = I64
+        L.or_build_csr_begin.argtypes = [I64, I64, P, I32, P, ctypes.POINTER(P)]
+        L.or_build_csr_begin.restype = I64
+        L.or_build_csr_take.argtypes = [P, P, P, P]
         L.or_degree_sort_rows.argtypes = [I64, P, P, P, P, I32]
-        L.or_rcm.argtypes = [I64, P, P, P, P, P, P]
-        L.or_rcm.restype = I64
+        L.or_rcm_k.argtypes = [I64, P, P, P, I64, P, P, P]
+        L.or_rcm_k.restype = I64
         L.or_apply_permutation.argtypes = [I64, P, P, P, P, P, P, P, P]
         L.or_seq_bfs.argtypes = [I64, P, P, I64, P, P, P, P]
         L.or_seq_bfs.restype = I64
         L.or_td_step.argtypes = [I64, P, P, P, I64, P, P, P, P]
         L.or_bu_step.argtypes = [I64, P, P, P, P, P, P, P]
-        L.or_hybrid_bfs.argtypes = [I64, P, P, P, I64, I32, I32, I32, I32, P, P, I64, ctypes.POINTER(D)]
-        L.or_hybrid_bfs.restype = I64
+        L.or_bfs_run.argtypes = [I64, P, P, P, P, I64, I32, I32, I32, I32, I32, P, P, P, I64, ctypes.POINTER(D)]
+        L.or_bfs_run.restype = I64
+        L.or_get_partitions.argtypes = [I64, I64, I64, P, P]
+        L.or_get_partitions.restype = I64
+        L.or_shrink_bounds.argtypes = [P, P, P, P]
+        U64 = ctypes.c_uint64
+        L.or_kronecker_generate.argtypes = [I32, I64, U64, D, D, D, I32, P]
+        L.or_chunglu_sample.argtypes = [P, I64, I64, U64, I32, P]
         L.or_components.argtypes = [I64, I64, P, I64, P, I64, P]
         L.or_validate.argtypes = [I64, P, P, P, I64, P, P, P]
         L.or_validate.restype = I32
@@ -88,18 +95,21 @@ class Csr:
         return int(self.dst.size)
 
 
-def build_csr(n: int, edges: np.ndarray) -> Csr:
+def build_csr(n: int, edges: np.ndarray, threads: int = 0) -> Csr:
+    """graph.py:85-120 (OpenMP, ``threads`` 0 = all)."""
     e = _c(np.asarray(edges).reshape(-1, 2), np.uint32)
     m = e.shape[0]
-    rs = np.zeros(n + 1, np.int64)
-    dst = np.empty(max(2 * m, 1), np.uint32)
-    deg = np.zeros(max(n, 1), np.int32)
     bad = np.zeros(1, np.int64)
-    md = lib().or_build_csr(n, m, _p(e), _p(rs), _p(dst), _p(deg), _p(bad))
+    h = ctypes.c_void_p(0)
+    md = lib().or_build_csr_begin(n, m, _p(e), int(threads), _p(bad), ctypes.byref(h))
     if md < 0:
         i = int(bad[0])
         raise ValueError(f"edge {i} = ({int(e[i, 0])}, {int(e[i, 1])}) out of range for n={n}")
-    return Csr(n, rs, dst[:md].copy(), deg[:n].copy())
+    rs = np.empty(n + 1, np.int64)
+    dst = np.empty(max(md, 1), np.uint32)
+    deg = np.empty(max(n, 1), np.int32)
+    lib().or_build_csr_take(h, _p(rs), _p(dst), _p(deg))
+    return Csr(n, rs, dst[:md], deg[:n])
 
 
 # ---------------------------------------------------------------------------
@@ -113,16 +123,30 @@ def degree_sort_rows(g: Csr, descending: bool) -> np.ndarray:
     return out
 
 
-def rcm(g: Csr):
-    """Returns (perm uint32 new->old, n_plus, component_ranges list) -- reorder.py:198-237."""
+def rcm(g: Csr, k: int | None = None):
+    """Returns (perm uint32 new->old, n_plus, component_ranges list) -- reorder.py:198-237.
+    ``k`` labels only (partial_rcm, reorder.py:240-251); ranges then end at k."""
     perm = np.empty(max(g.n, 1), np.uint32)
     cs = np.empty(g.n + 1, np.int64)
     npl = np.zeros(1, np.int64)
-    nc = lib().or_rcm(g.n, _p(g.row_starts), _p(g.dst), _p(g.degrees), _p(perm), _p(cs), _p(npl))
-    k = int(npl[0])
+    nc = lib().or_rcm_k(g.n, _p(g.row_starts), _p(g.dst), _p(g.degrees), -1 if k is None else int(k), _p(perm),
+                        _p(cs), _p(npl))
+    k = int(npl[0]) if k is None else min(int(k), int(npl[0]))
+    if k == 0:
+        return perm[: g.n].copy(), int(npl[0]), []
     bounds = np.append(cs[:nc], k)
     ranges = [(int(k - bounds[i + 1]), int(k - bounds[i])) for i in range(nc - 1, -1, -1)]
-    return perm[: g.n].copy(), k, ranges
+    return perm[: g.n].copy(), int(npl[0]), ranges
+
+
+def partial_rcm(g: Csr, p: float):
+    """reorder.py:240-251: the walk stops after ceil(p * |V+|) labels."""
+    import math
+
+    if not 0.0 < p <= 1.0:
+        raise ValueError(f"p must be in (0, 1], got {p}")
+    deg_pos = int(np.count_nonzero(g.degrees > 0))
+    return rcm(g, min(math.ceil(p * deg_pos), deg_pos))
 
 
 def inverse(perm: np.ndarray) -> np.ndarray:
@@ -158,20 +182,59 @@ def seq_bfs(g: Csr, source: int):
     return parent, level, int(nl), bounds[: nl + 1].copy()
 
 
-def hybrid_bfs(g: Csr, source: int, alpha=64, beta=8, hybrid=True, threads=0):
-    """Multithreaded restatement of BfsEngine.run mode hybrid/level_sync.
+MODE_CODES = {"level_sync": 0, "hybrid": 1, "hybrid_balanced": 2, "hybrid_reduced": 3}
 
-    Returns (parent, records ndarray (L,6): level, dir(0 TD/1 BU), n_f, m_f,
-    m_u, scanned; elapsed seconds)."""
-    parent = np.empty(g.n, np.int32)
-    cap = max(64, g.n + 2)
-    rec = np.zeros((min(cap, 1 << 16), 6), np.int64)
+
+def bfs_run(g: Csr, source: int, mode: str = "hybrid", alpha=64, beta=8, threads=0, partition_factor=None,
+            g_desc_dst: np.ndarray | None = None, want_levels: bool = False):
+    """BfsEngine.run (engine.py:518-604) in every mode but "sequential",
+    OpenMP with ``threads`` workers (0 = all; = the reference's params.threads,
+    so the partition count is partition_factor * threads).
+
+    Returns (parent, levels or None, records ndarray (L, 9): level, dir (0 TD /
+    1 BU), n_f, m_f, m_u, scanned, pass1_hits, live_vertices, claimed (-1 =
+    None), elapsed seconds)."""
+    code = MODE_CODES[mode]
+    if code == 3 and g_desc_dst is None:
+        g_desc_dst = degree_sort_rows(g, True)
+    if threads <= 0:
+        threads = os.cpu_count() or 1
+    if partition_factor is None:
+        partition_factor = 20
+    parent = np.empty(max(g.n, 1), np.int32)
+    level = np.empty(max(g.n, 1), np.int32) if want_levels else None
+    cap = min(max(64, g.n + 2), 1 << 16)
+    rec = np.zeros((cap, 9), np.int64)
     el = ctypes.c_double(0.0)
-    nl = lib().or_hybrid_bfs(
-        g.n, _p(g.row_starts), _p(g.dst), _p(g.degrees), int(source), int(alpha), int(beta),
-        int(bool(hybrid)), int(threads), _p(parent), _p(rec), rec.shape[0], ctypes.byref(el),
+    nl = lib().or_bfs_run(
+        g.n, _p(g.row_starts), _p(g.dst), _p(g_desc_dst) if g_desc_dst is not None else None, _p(g.degrees),
+        int(source), int(alpha), int(beta), code, int(partition_factor), int(threads), _p(parent),
+        _p(level) if level is not None else None, _p(rec), cap, ctypes.byref(el),
     )
-    return parent, rec[: min(nl, rec.shape[0])].copy(), el.value
+    return parent[: g.n], None if level is None else level[: g.n], rec[: min(nl, cap)].copy(), el.value
+
+
+def hybrid_bfs(g: Csr, source: int, alpha=64, beta=8, hybrid=True, threads=0):
+    """mode hybrid (or level_sync): (parent, records (L, 6): level, dir, n_f, m_f, m_u, scanned, elapsed)."""
+    parent, _, rec, el = bfs_run(g, source, "hybrid" if hybrid else "level_sync", alpha, beta, threads)
+    return parent, rec[:, :6].copy(), el
+
+
+def get_partitions(n: int, partition_factor: int, threads: int):
+    """partition.py:98-140 -> (starts, ends) int64."""
+    cap = max(1, partition_factor * threads)
+    st = np.empty(cap, np.int64)
+    en = np.empty(cap, np.int64)
+    k = lib().or_get_partitions(n, partition_factor, threads, _p(st), _p(en))
+    return st[:k].copy(), en[:k].copy()
+
+
+def shrink_bounds(vis_words: np.ndarray, ext_words: np.ndarray, lo: int, hi: int):
+    """partition.py:143-171 over uint64 words."""
+    a = np.array([lo], np.int64)
+    b = np.array([hi], np.int64)
+    lib().or_shrink_bounds(_p(_c(vis_words, np.uint64)), _p(_c(ext_words, np.uint64)), _p(a), _p(b))
+    return int(a[0]), int(b[0])
 
 
 def td_step(g: Csr, frontier: np.ndarray, visited_words: np.ndarray, parent: np.ndarray):
@@ -256,8 +319,19 @@ def scramble_ids(ids, scale: int, seed: int) -> np.ndarray:  # generator.py:96-1
     return x
 
 
-def kronecker_generate(scale: int, edgefactor: int = 16, initiator=(0.57, 0.19, 0.19, 0.05), seed: int = 1):
-    """(n, edges uint32 (m,2)) -- generator.py:114-148."""
+def kronecker_generate(scale: int, edgefactor: int = 16, initiator=(0.57, 0.19, 0.19, 0.05), seed: int = 1,
+                       threads: int = 0):
+    """(n, edges uint32 (m,2)) -- generator.py:114-148, C + OpenMP restatement
+    (pinned against kronecker_generate_numpy and the reference's hashes)."""
+    a, b, c, _ = initiator
+    n = 1 << scale
+    out = np.empty((n * edgefactor, 2), dtype=np.uint32)
+    lib().or_kronecker_generate(scale, edgefactor, seed, float(a), float(b), float(c), int(threads), _p(out))
+    return n, out
+
+
+def kronecker_generate_numpy(scale: int, edgefactor: int = 16, initiator=(0.57, 0.19, 0.19, 0.05), seed: int = 1):
+    """(n, edges uint32 (m,2)) -- generator.py:114-148 with numpy's own Philox."""
     a, b, c, _ = initiator
     t1, t2, t3 = a, a + b, a + b + c
     n = 1 << scale
@@ -288,7 +362,22 @@ def _mulhi64(x: np.ndarray, t: int) -> np.ndarray:
 
 
 def chunglu_generate(n: int, avg_degree: int = 20, gamma: float = 2.1, w_min: float = 1.0, cap_frac: float = 0.01,
-                     seed: int = 7):
+                     seed: int = 7, threads: int = 0):
+    """Chung-Lu recipe: weights in numpy (float step), sampling in C + OpenMP
+    (pinned against chunglu_generate_numpy)."""
+    rng = np.random.Generator(np.random.Philox(key=np.array([seed, (1 << 32) - 1], dtype=np.uint64)))
+    u = rng.random(n)
+    cap = float(max(1, int(cap_frac * n)))
+    w = np.minimum(cap, w_min * (1.0 - u) ** (-1.0 / (gamma - 1.0)))
+    prefix = np.cumsum(np.floor(w * 1024.0).astype(np.int64))
+    m = n * avg_degree // 2
+    out = np.empty((m, 2), dtype=np.uint32)
+    lib().or_chunglu_sample(_p(prefix), n, m, seed, int(threads), _p(out))
+    return n, out
+
+
+def chunglu_generate_numpy(n: int, avg_degree: int = 20, gamma: float = 2.1, w_min: float = 1.0,
+                           cap_frac: float = 0.01, seed: int = 7):
     """(n, edges uint32 (m,2)): numpy restatement of the Chung-Lu recipe
     (BASELINE configs[4]; no reference generator exists -- the recipe is
     stated in paper_2012_10026_b200/generator.py::ChungLuParams)."""

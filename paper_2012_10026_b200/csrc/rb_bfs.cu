@@ -1876,6 +1876,12 @@ static const void* bfs_kernel(const rb_bfs* h) {
   return small ? (const void*)bfs_persistent<false, 4> : (const void*)bfs_persistent<false, 8>;
 }
 
+// RB_ERR_ARG with a message for a null handle / argument (every ARG path sets the error text)
+static int rb_null_handle(const char* fn) {
+  rb_set_error("%s: invalid (null) handle or argument", fn);
+  return RB_ERR_ARG;
+}
+
 static int alloc_dev(void** p, size_t bytes) {
   cudaError_t e = cudaMalloc(p, bytes ? bytes : 16);
   if (e != cudaSuccess) {
@@ -2068,7 +2074,7 @@ extern "C" int rb_bfs_destroy(rb_bfs* h) {
 extern "C" int32_t* rb_bfs_parent_ptr(rb_bfs* h) { return h ? h->kp.parent : nullptr; }
 extern "C" int32_t* rb_bfs_level_ptr(rb_bfs* h) { return h ? h->kp.level : nullptr; }
 extern "C" int rb_bfs_grid(rb_bfs* h, int* blocks, int* threads) {
-  if (!h) return RB_ERR_ARG;
+  if (!h) return rb_null_handle(__func__);
   if (blocks) *blocks = h->blocks;
   if (threads) *threads = kThreads;
   return RB_OK;
@@ -2091,7 +2097,7 @@ static int reset_common(rb_bfs* h, cudaStream_t s) {
 }
 
 extern "C" int rb_bfs_reset(rb_bfs* h, int64_t source, void* stream) {
-  if (!h) return RB_ERR_ARG;
+  if (!h) return rb_null_handle(__func__);
   if (source < 0 || source >= h->n_dev) {
     rb_set_error("source %lld out of range for n_dev=%lld", (long long)source, (long long)h->n_dev);
     return RB_ERR_ARG;
@@ -2118,7 +2124,9 @@ static int launch(rb_bfs* h, cudaStream_t s, int64_t level0, int64_t dir0, int64
   kp.src = h->source;
   kp.m_directed = h->prm.m_directed;
   kp.from_fin = from_fin;
-  kp.exec_opt = (exec && h->exec_opt) ? 1 : 0;
+  // the cost-model execution (a level may run the other way) only in hybrid
+  // modes: level_sync / sequential are top-down only (engine.py use_dir)
+  kp.exec_opt = (exec && h->exec_opt && h->prm.hybrid) ? 1 : 0;
   kp.reached0 = reached0;
   kp.probe_mf = h->probe_mf;
   kp.defer_mf = h->defer_mf;
@@ -2135,7 +2143,7 @@ static int launch(rb_bfs* h, cudaStream_t s, int64_t level0, int64_t dir0, int64
 }
 
 extern "C" int rb_bfs_traverse(rb_bfs* h, void* stream) {
-  if (!h) return RB_ERR_ARG;
+  if (!h) return rb_null_handle(__func__);
   h->launched = true;
   h->stream = stream;
   RB_CUDA_TRY(cudaEventRecord(h->ev_start, (cudaStream_t)stream));
@@ -2147,7 +2155,7 @@ extern "C" int rb_bfs_traverse(rb_bfs* h, void* stream) {
 
 extern "C" int rb_bfs_results(rb_bfs* h, int32_t* parent_out, int32_t* level_out, rb_level_record* h_records,
                               int64_t cap, int64_t* n_records, void* stream) {
-  if (!h) return RB_ERR_ARG;
+  if (!h) return rb_null_handle(__func__);
   if (level_out && !h->kp.level) {
     rb_set_error("rb_bfs_results: engine created without record_levels");
     return RB_ERR_ARG;
@@ -2196,7 +2204,10 @@ extern "C" int rb_bfs_results(rb_bfs* h, int32_t* parent_out, int32_t* level_out
 // the caller drains with rb_bfs_results (very deep graphs: continuations).
 extern "C" int rb_bfs_results_async(rb_bfs* h, void* h_state, rb_level_record* h_records, int64_t cap,
                                     int32_t* h_parent, int32_t chunks, void* stream) {
-  if (!h || !h_state || (cap > 0 && !h_records) || chunks < 0 || chunks > kMaxChunks) return RB_ERR_ARG;
+  if (!h || !h_state || (cap > 0 && !h_records) || chunks < 0 || chunks > kMaxChunks) {
+    rb_set_error("rb_bfs_results_async: invalid argument (chunks %d, allowed 0..%d)", (int)chunks, kMaxChunks);
+    return RB_ERR_ARG;
+  }
   cudaStream_t s = (cudaStream_t)stream;
   RB_CUDA_TRY(cudaMemcpyAsync(h_state, h->kp.fin, sizeof(Final), cudaMemcpyDeviceToHost, s));
   if (cap > 0)
@@ -2218,14 +2229,20 @@ extern "C" int rb_bfs_results_async(rb_bfs* h, void* h_state, rb_level_record* h
 // Wait for the async result copies: what = -1 the launch state + records,
 // what = i the parent chunk i.
 extern "C" int rb_bfs_wait(rb_bfs* h, int32_t what) {
-  if (!h || what < -1 || what >= kMaxChunks) return RB_ERR_ARG;
+  if (!h || what < -1 || what >= kMaxChunks) {
+    rb_set_error("rb_bfs_wait: invalid argument (what %d, allowed -1..%d)", (int)what, kMaxChunks - 1);
+    return RB_ERR_ARG;
+  }
   RB_CUDA_TRY(cudaEventSynchronize(h->ev_chunk[what < 0 ? kMaxChunks : what]));
   return RB_OK;
 }
 
 extern "C" int rb_bfs_complete(rb_bfs* h, const void* h_state, const rb_level_record* h_records, int64_t cap,
                                int64_t* n_records) {
-  if (!h || !h_state || !n_records) return RB_ERR_ARG;
+  if (!h || !h_state || !n_records) {
+    rb_set_error("rb_bfs_complete: invalid argument");
+    return RB_ERR_ARG;
+  }
   Final f;
   memcpy(&f, h_state, sizeof(Final));
   if (!h->launched || f.nf > 0 || f.levels_done > cap) return 1;
@@ -2273,7 +2290,7 @@ extern "C" int rb_bfs_step(rb_bfs* h, int direction, const uint32_t* d_visited_w
 }
 
 extern "C" int rb_bfs_barrier_probe(rb_bfs* h, int iters, double* ns_per_barrier, void* stream) {
-  if (!h || iters <= 0) return RB_ERR_ARG;
+  if (!h || iters <= 0) return rb_null_handle(__func__);
   cudaStream_t s = (cudaStream_t)stream;
   RB_CUDA_TRY(cudaMemsetAsync(h->kp.bar, 0, 64, s));
   cudaEvent_t a, b;
@@ -2295,7 +2312,7 @@ extern "C" int rb_bfs_barrier_probe(rb_bfs* h, int iters, double* ns_per_barrier
 }
 
 extern "C" int rb_bfs_debug_timestamps(rb_bfs* h, uint64_t* out, int64_t cap, int* blocks) {
-  if (!h || !h->kp.dbg) return RB_ERR_ARG;
+  if (!h || !h->kp.dbg) return rb_null_handle(__func__);
   const int64_t n = (int64_t)kDbgWarpBase + (int64_t)64 * h->blocks * kWarps;  // see kDbgWarpBase
   RB_CUDA_TRY(cudaMemcpy(out, h->kp.dbg, (size_t)(n < cap ? n : cap) * 8, cudaMemcpyDeviceToHost));
   *blocks = h->blocks;
@@ -2303,7 +2320,7 @@ extern "C" int rb_bfs_debug_timestamps(rb_bfs* h, uint64_t* out, int64_t cap, in
 }
 
 extern "C" int rb_bfs_elapsed(rb_bfs* h, double* seconds) {
-  if (!h || !seconds) return RB_ERR_ARG;
+  if (!h || !seconds) return rb_null_handle(__func__);
   float ms = 0.f;
   RB_CUDA_TRY(cudaEventSynchronize(h->ev_end));
   RB_CUDA_TRY(cudaEventElapsedTime(&ms, h->ev_start, h->ev_end));
@@ -2320,7 +2337,7 @@ extern "C" int rb_bfs_create(const int64_t* d_row_starts, const int32_t* d_col, 
 // ---- 1D-partition levels: the host drives the level loop and the exchange ----
 
 extern "C" int rb_bfs_reset_part(rb_bfs* h, int64_t source_global, void* stream) {
-  if (!h) return RB_ERR_ARG;
+  if (!h) return rb_null_handle(__func__);
   cudaStream_t s = (cudaStream_t)stream;
   int rc = reset_common(h, s);
   if (rc) return rc;
@@ -2382,7 +2399,7 @@ extern "C" int rb_bfs_dist_level(rb_bfs* h, int64_t level, int direction, int hu
 }
 
 extern "C" int rb_bfs_words(rb_bfs* h, int64_t* n_words_local, int64_t* n_words_glob) {
-  if (!h) return RB_ERR_ARG;
+  if (!h) return rb_null_handle(__func__);
   if (n_words_local) *n_words_local = h->n_words;
   if (n_words_glob) *n_words_glob = h->kp.n_words_glob;
   return RB_OK;

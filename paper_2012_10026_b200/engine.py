@@ -232,6 +232,9 @@ class _DeviceBfs:
             col_bu = g_bu.device_arrays()[1]
             self._keep.append(col_bu)
         prm = _lib.BfsParamsC(alpha, beta, int(hybrid), int(bu_reverse), n, g.m_directed, int(record_levels), 0)
+        # rb_bfs_create reads deg / iso from its own (legacy default) stream:
+        # the torch work above must have landed, whatever stream it ran on
+        torch.cuda.current_stream().synchronize()
         _lib.check(
             L.rb_bfs_create(_lib.ptr(rs), _lib.ptr(col), _lib.ptr(col_bu), _lib.ptr(deg), n_dev,
                             _lib.ptr(iso) if iso is not None else None, ctypes.byref(prm), ctypes.byref(self.h)),
@@ -299,8 +302,11 @@ class _DeviceBfs:
             self._state = torch.empty(int(L.rb_bfs_state_bytes()) // 8, dtype=torch.int64, pin_memory=True)
             self._recs_pin = torch.empty(_REC_FAST * 10, dtype=torch.int64, pin_memory=True)
         n_dev = self.n_dev
-        # 8 pieces (the ABI maximum): measured best at s22 and s26 (1 / 2 / 4 / 8 -> 128 / 146 / 156 / 159 e2e GTEPS at s22)
+        # 8 pieces by default (the ABI accepts 1..32): measured best at s22 and s26
+        # (1 / 2 / 4 / 8 -> 128 / 146 / 156 / 159 e2e GTEPS at s22; 16 / 32 lose)
         chunks = chunks or int(os.environ.get("RB_E2E_CHUNKS", "0")) or 8
+        if not 1 <= chunks <= _MAX_CHUNKS:
+            raise ValueError(f"result chunks must be in [1, {_MAX_CHUNKS}], got {chunks}")
         _lib.check(L.rb_bfs_results_async(self.h, _lib.ptr(self._state), _lib.ptr(self._recs_pin), _REC_FAST,
                                           _lib.ptr(self.pinned), chunks, s), "rb_bfs_results_async")
         pred = fresh_int32(n)
@@ -356,6 +362,7 @@ class _DeviceBfs:
         return ptr
 
 
+_MAX_CHUNKS = 32  # kMaxChunks of rb_bfs.cu (rb_bfs_results_async)
 _REC_FAST = 64  # level records fetched by the async result path (deeper: drained)
 
 
@@ -585,7 +592,7 @@ def _run_step(g: CsrGraph, direction: int, frontier: Frontier, visited: Bitmap, 
                                ctr.ctypes.data_as(ctypes.c_void_p), _lib.stream_ptr()),
         "rb_bfs_step",
     )
-    visited.words.view(np.uint32)[:nw] = vis_out.cpu().numpy().view(np.uint32)
+    visited.w32[:nw] = vis_out.cpu().numpy().view(np.uint32)
     parent[:] = par_out.cpu().numpy()
     nxt = Bitmap.from_words32(n, nxt_out.cpu().numpy().view(np.uint32))
     return nxt, ctr

@@ -5,6 +5,7 @@ from __future__ import annotations
 
 import ctypes
 import hashlib
+import math
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -16,6 +17,7 @@ __all__ = [
     "Permutation",
     "RcmRunStats",
     "rcm",
+    "partial_rcm",
     "apply_permutation",
     "degree_sort_adjacency",
     "graph_hash",
@@ -131,6 +133,43 @@ def rcm(g: CsrGraph) -> tuple[Permutation, RcmRunStats]:
         n=n, n_non_isolated=n_plus.value, n_assigned=n_plus.value,
         component_ranges=[(int(a), int(b)) for a, b in rr],
     )
+    return Permutation(_dev=(perm, inv)), stats
+
+
+def partial_rcm(g: CsrGraph, p: float) -> tuple[Permutation, RcmRunStats]:
+    """RCM truncated after ``ceil(p * |V+|)`` labels (reorder.py:240-251);
+    ``p = 1`` is exactly :func:`rcm`.
+
+    The truncated walk labels the first k vertices of the full Cuthill-McKee
+    order, so on device the partial permutation is the full one's slice
+    ``perm[|V+| - k : |V+|]`` (the reversed prefix), then the unlabelled
+    non-isolated vertices in ascending original id, then the isolated tail
+    (reorder.py:219-220).  Components whose discovery started before k keep
+    their ranges, the last one cut at k."""
+    if not 0.0 < p <= 1.0:
+        raise ValueError(f"p must be in (0, 1], got {p}")
+    torch = _lib.require_cuda()
+    full, st = rcm(g)
+    n, n_plus = g.n, st.n_non_isolated
+    k = min(math.ceil(p * n_plus), n_plus)
+    if k == n_plus:
+        return full, st
+    fp, _ = full.device_arrays()
+    deg = g.device_arrays()[2]
+    placed = torch.zeros(max(n, 1), dtype=torch.bool, device="cuda")
+    pre = fp[n_plus - k: n_plus]
+    placed[pre.long()] = True
+    rest = torch.nonzero((deg > 0) & ~placed[:n]).reshape(-1).to(torch.int32)  # ascending id
+    perm = torch.cat([pre, rest, fp[n_plus:]])
+    inv = torch.empty_like(perm)
+    inv[perm.long()] = torch.arange(n, dtype=torch.int32, device="cuda")
+    ranges = []
+    for a, b in st.component_ranges:  # full new-id range (a, b) = discovery [n_plus - b, n_plus - a)
+        ds, de = n_plus - b, n_plus - a
+        if ds < k:
+            ranges.append((k - min(de, k), k - ds))
+    ranges.sort()
+    stats = RcmRunStats(n=n, n_non_isolated=n_plus, n_assigned=k, component_ranges=ranges if k else [])
     return Permutation(_dev=(perm, inv)), stats
 
 

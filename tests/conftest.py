@@ -101,3 +101,30 @@ def validate_cases(golden):
         gi, src = (int(x) for x in arr[f"c{i}_graph"])
         yield (int(arr[f"g{gi}_n"][0]), arr[f"g{gi}_edges"], src, arr[f"c{i}_parent"], arr[f"c{i}_checks"].tolist(),
                arr[f"c{i}_levels"], details[i])
+
+
+@pytest.fixture(scope="session")
+def golden_modes():
+    with open(os.path.join(GOLDEN, "modes.json")) as f:
+        return json.load(f)
+
+
+@pytest.fixture(scope="session")
+def golden_partial():
+    with open(os.path.join(GOLDEN, "partial.json")) as f:
+        return json.load(f)
+
+
+def mode_records(recs_or_rows, from_oracle: bool):
+    """[dir, n_f, m_f, m_u, scanned, pass1_hits, live_vertices, claimed] rows
+    (None for the reference's absent fields) from oracle rows or LevelRecords."""
+    out = []
+    for r in recs_or_rows:
+        if from_oracle:
+            d, nf, mf, mu, sc, p1, lv, cl = (int(x) for x in r[1:9])
+            out.append(["T" if d == 0 else "B", nf, mf, mu, sc, None if p1 < 0 else p1, None if lv < 0 else lv,
+                        None if cl < 0 else cl])
+        else:
+            out.append(["T" if r.direction == "top_down" else "B", r.n_f, r.m_f, r.m_u, r.scanned_edges,
+                        r.pass1_hits, r.live_vertices, r.claimed])
+    return out

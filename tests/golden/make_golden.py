@@ -218,6 +218,84 @@ def validate_fixtures():
     print("validate", i, flush=True)
 
 
+def mode_fixtures():
+    """Full LevelRecords of the partitioned modes (hybrid_balanced: bu_steal;
+    hybrid_reduced: Alg. 6 two-pass bu_reduced on the descending adjacency)
+    incl. scanned / pass1_hits / live_vertices / claimed, for several thread
+    counts and partition factors (engine.py:478-604, partition.py)."""
+    from rcmbfs import degree_sort_adjacency
+
+    out = {}
+    for scale, seed in ((12, 1), (14, 3), (16, 1)):
+        el = kronecker_generate(KroneckerParams(scale=scale, edgefactor=16, seed=seed))
+        g = build_csr(el)
+        perm, _ = rcm(g)
+        g2 = apply_permutation(g, perm)
+        gd = degree_sort_adjacency(g2, "descending")
+        srcs = [int(s) for s in _sample_sources(g2, 6, 3)]
+        cases = []
+        for mode in ("hybrid_reduced", "hybrid_balanced"):
+            for threads, lam in ((1, 20), (3, 10), (4, 1)):
+                params = BfsParams(mode=mode, threads=threads, partition_factor=lam)
+                with rcmbfs.BfsEngine(g2, params, g_desc=gd) as eng:
+                    for s in srcs:
+                        res = eng.run(s)
+                        cases.append({
+                            "mode": mode, "threads": threads, "partition_factor": lam, "source": s,
+                            "records": [["T" if r.direction == rcmbfs.TOP_DOWN else "B", r.n_f, r.m_f, r.m_u,
+                                         r.scanned_edges, r.pass1_hits, r.live_vertices, r.claimed]
+                                        for r in res.levels],
+                        })
+        out[f"{scale},{seed}"] = cases
+        print("modes", scale, seed, len(cases), flush=True)
+    with open(os.path.join(HERE, "modes.json"), "w") as f:
+        json.dump(out, f, indent=0, sort_keys=True)
+
+
+def partial_fixtures():
+    """partial_rcm (reorder.py:240-251) perms and stats, get_partitions and
+    shrink_partition (partition.py:67-178) on random bitmaps."""
+    from rcmbfs import get_partitions, partial_rcm, shrink_partition
+
+    out = {"partial": [], "partitions": [], "shrink": []}
+    for scale, seed in ((12, 1), (14, 3)):
+        g = build_csr(kronecker_generate(KroneckerParams(scale=scale, edgefactor=16, seed=seed)))
+        for p in (0.05, 0.3, 0.5, 0.999, 1.0):
+            perm, st = partial_rcm(g, p)
+            out["partial"].append({"scale": scale, "seed": seed, "p": p, "perm_sha256": sha(perm.perm),
+                                   "n_assigned": st.n_assigned, "ranges": [list(r) for r in st.component_ranges]})
+    rng = np.random.default_rng(5)
+    import warnings
+    for n, lam, t in ((1, 1, 1), (511, 2, 2), (512, 1, 1), (10000, 10, 4), (1 << 16, 20, 1), (1 << 16, 10, 16),
+                      (123457, 7, 3), (5000, 20, 8)):
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            ps = get_partitions(n, lam, t)
+        out["partitions"].append({"n": n, "factor": lam, "threads": t, "starts": ps.starts.tolist(),
+                                  "ends": ps.ends.tolist()})
+    for case in range(40):
+        n = int(rng.integers(1, 20000))
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            ps = get_partitions(n, int(rng.integers(1, 8)), int(rng.integers(1, 4)))
+        vis = Bitmap(n)
+        full_blocks = rng.random(vis.n_blocks) < rng.choice([0.3, 0.8, 1.0])
+        idx = np.concatenate([np.arange(b * 512, min(n, (b + 1) * 512)) for b in np.flatnonzero(full_blocks)]
+                             + [rng.integers(0, n, size=n // 7)]).astype(np.int64)
+        if idx.size:
+            vis.set_many(idx)
+        res = []
+        for i in range(ps.n_partitions):
+            res.append(list(shrink_partition(ps, i, vis)))
+        out["shrink"].append({"n": n, "starts": ps.starts.tolist(), "ends": ps.ends.tolist(),
+                              "set": np.unique(idx).tolist() if idx.size < 3000 else None,
+                              "set_sha256": sha(vis.words), "words": vis.words.view(np.uint64).tolist()
+                              if vis.words.size <= 400 else None, "result": res})
+    with open(os.path.join(HERE, "partial.json"), "w") as f:
+        json.dump(out, f, indent=0, sort_keys=True)
+    print("partial", len(out["partial"]), len(out["partitions"]), len(out["shrink"]), flush=True)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["gen", "small", "kron", "validate"]
     if "validate" in which:
@@ -226,6 +304,17 @@ if __name__ == "__main__":
         gen_fixtures()
     if "small" in which:
         small_fixtures()
+    if "modes" in which:
+        mode_fixtures()
+    if "partial" in which:
+        partial_fixtures()
+    if "s22" in which:  # BASELINE configs[1]: appended to kron.json (reference build ~4 min)
+        path = os.path.join(HERE, "kron.json")
+        with open(path) as f:
+            data = json.load(f)
+        data.update(kron_fixtures([(22, 1, 8)]))
+        with open(path, "w") as f:
+            json.dump(data, f, indent=0, sort_keys=True)
     if "kron" in which:
         plan = [(12, 1, 16), (14, 3, 16), (16, 1, 64), (18, 1, 16)]
         if "big" in which:

@@ -82,6 +82,24 @@ def test_modes_agree(cuda_ok, ocache):
             e.close()
 
 
+def test_level_sync_runs_top_down_only(cuda_ok, ocache):
+    """level_sync / sequential never run a bottom-up level (engine.py use_dir =
+    TOP_DOWN when hybrid is off): every record is labelled AND executed
+    top-down, and a top-down level scans exactly its frontier edges."""
+    for scale, seed in ((14, 3), (16, 1)):
+        g2 = ocache.kron(scale, seed)["g2"]
+        g = to_rb(g2)
+        for mode in ("level_sync", "sequential"):
+            with rb.BfsEngine(g, rb.BfsParams(mode=mode)) as eng:
+                for s in oracle.sample_sources(g2.degrees, 6, scale):
+                    res = eng.run(int(s))
+                    _, rec, _ = oracle.hybrid_bfs(g2, int(s), hybrid=False)
+                    assert [(r.n_f, r.m_f, r.m_u) for r in res.levels] == [tuple(int(x) for x in row[2:5]) for row in rec]
+                    for r in res.levels:
+                        assert r.direction == rb.TOP_DOWN and r.executed_direction == rb.TOP_DOWN, (mode, s, r)
+                        assert r.scanned_edges == r.m_f, (mode, s, r)
+
+
 def test_direction_patterns_known_answer(cuda_ok, ocache):
     # test_engine.py:406-420
     g2 = ocache.kron(12)["g2"]
