@@ -88,6 +88,17 @@ typedef struct {
   int64_t n_next;
   int64_t t_queue_ns;    /* part of t_ns before the top-down hub phase (phase A) */
   int64_t reserved;      /* executed direction: 0 = top_down, 1 = bottom_up */
+  /* LevelRecord fields of the partitioned modes (engine.py:166-180), -1 = None:
+   * pass1_hits: bottom-up vertices found by their first scanned neighbour
+   * (bu_reduced pass 1, _kernels.py:254-266; counted when the engine was given
+   * RB_PART_COUNT_PASS1); live_vertices: PartitionSet.live_total() after the
+   * bottom-up level (partition.py:70-72, live bounds shrunk past all-visited
+   * 512-vertex blocks; RB_PART_SHRINK); claimed: partitions claimed (set by
+   * the host shim: every partition is claimed once per bottom-up step). */
+  int64_t pass1_hits;
+  int64_t live_vertices;
+  int64_t claimed;
+  int64_t reserved2;
 } rb_level_record;
 
 typedef struct {
@@ -142,6 +153,19 @@ size_t rb_transpose_workspace_bytes(int64_t m_local, int64_t n_glob);
 int rb_transpose_rows(const int64_t* d_row_starts_local, const int32_t* d_col_local, int64_t n_local, int64_t v_lo,
                       int64_t m_local, int64_t n_glob, void* d_ws, size_t ws_bytes, int64_t* d_td_row_starts,
                       int32_t* d_td_col, void* stream);
+/* Partition bookkeeping of the reference's partitioned modes (hybrid_balanced,
+ * hybrid_reduced; engine.py:499-500, partition.py:67-171).  h_bounds: n_parts+1
+ * vertex boundaries of get_partitions(n_full, partition_factor, threads)
+ * (host memory; starts 512-aligned, last = n_full = g.n).  flags:
+ *   RB_PART_EXACT        every level runs the direction the policy labels (no
+ *                        cost-model execution), so scanned_edges is the
+ *                        reference's count for the scan order given;
+ *   RB_PART_COUNT_PASS1  records carry pass1_hits;
+ *   RB_PART_SHRINK       records carry live_vertices (bounds shrunk as
+ *                        bu_reduced does).
+ * n_parts = 0 clears it. */
+enum { RB_PART_EXACT = 1, RB_PART_COUNT_PASS1 = 2, RB_PART_SHRINK = 4 };
+int rb_bfs_set_partitions(rb_bfs* h, const int64_t* h_bounds, int64_t n_parts, int64_t n_full, int32_t flags);
 /* Reset per-root state (not timed; engine.py:526-532). */
 int rb_bfs_reset(rb_bfs* h, int64_t source, void* stream);
 /* The traversal (engine.py:534-598): one cooperative persistent launch. */

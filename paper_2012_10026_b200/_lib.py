@@ -13,6 +13,7 @@ import threading
 from . import _build
 
 RB_OK, RB_ERR_ARG, RB_ERR_CUDA, RB_ERR_NCCL, RB_ERR_OOM = 0, 1, 2, 3, 4
+RB_PART_EXACT, RB_PART_COUNT_PASS1, RB_PART_SHRINK = 1, 2, 4
 
 _lock = threading.Lock()
 _lib = None
@@ -27,6 +28,7 @@ class LevelRecordC(ctypes.Structure):
     _fields_ = [
         ("level", I64), ("direction", I64), ("n_f", I64), ("m_f", I64), ("m_u", I64),
         ("scanned_edges", I64), ("t_ns", I64), ("n_next", I64), ("t_queue_ns", I64), ("reserved", I64),
+        ("pass1_hits", I64), ("live_vertices", I64), ("claimed", I64), ("reserved2", I64),
     ]
 
 
@@ -65,6 +67,7 @@ _SIGS = {
     "rb_transpose_workspace_bytes": ([I64, I64], SZ),
     "rb_transpose_rows": ([P, P, I64, I64, I64, I64, P, SZ, P, P, P], ctypes.c_int),
     "rb_bfs_reset": ([P, I64, P], ctypes.c_int),
+    "rb_bfs_set_partitions": ([P, P, I64, I64, I32], ctypes.c_int),
     "rb_bfs_traverse": ([P, P], ctypes.c_int),
     "rb_bfs_elapsed": ([P, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
     "rb_bfs_results": ([P, P, P, P, I64, ctypes.POINTER(I64), P], ctypes.c_int),

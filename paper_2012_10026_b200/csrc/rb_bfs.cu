@@ -213,6 +213,13 @@ struct KParams {
   int64_t m_directed;
   int64_t n_active;  // non-isolated vertices in [0, n_dev) (executed-direction cost model)
   int64_t reached0;  // vertices discovered before this launch
+  // partitioned modes (rb_bfs_set_partitions): pass-1 hit count, live bounds
+  int64_t count_p1;            // bottom-up: count vertices found by their first scanned neighbour
+  int64_t n_parts;             // > 0: live_vertices per bottom-up level (partition.py shrink rule)
+  int64_t n_full;              // g.n: the reference's bitmap size (isolated tail included)
+  const int32_t* part_blk;     // n_parts + 1 partition bounds in 512-vertex blocks (last: ceil(n_full / 512))
+  int32_t* part_first;         // per partition: first / last block that is not all visited (reset to
+  int32_t* part_last;          //   INT_MAX / -1 after every use)
 };
 
 __device__ __forceinline__ uint32_t* fb_of(const KParams& p, int r) {  // r = level % 3
@@ -786,7 +793,7 @@ __device__ __forceinline__ int32_t bu_heavy(const KParams& p, const uint32_t* fc
 template <bool kRev, int KB, bool kCollect>
 RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uint32_t* fnext, uint8_t* nznext,
                          Acc& acc, uint32_t* s_found, uint32_t* s_pair, uint32_t* s_next, uint32_t* ulist,
-                         unsigned long long* ulist_count) {
+                         unsigned long long* ulist_count, uint32_t* s_p1) {
   const uint32_t lane = rb::lane_id();
   const uint64_t nw = (uint64_t)p.n_words;
   int32_t* const level_out = p.level;
@@ -968,7 +975,7 @@ RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uin
       hb1[k] = hv[k].y >= 0 ? ld_bits(fcur + (hv[k].y >> 5)) : 0u;
     }
     // branch-free resolution, 32-bit step-local counters
-    uint32_t foundm = 0, needm = 0, checks = 0, dsum = 0, dmax = 0;
+    uint32_t foundm = 0, needm = 0, checks = 0, dsum = 0, dmax = 0, h0m = 0;
     int32_t* const par_out = p.parent + vbase;
 #pragma unroll
     for (int k = 0; k < KB; ++k) {
@@ -976,6 +983,7 @@ RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uin
       const bool h0 = act && hv[k].x >= 0 && ((hb0[k] >> (hv[k].x & 31)) & 1u);
       const bool h1 = act && !h0 && hv[k].y >= 0 && ((hb1[k] >> (hv[k].y & 31)) & 1u);
       const bool found = h0 || h1;
+      h0m += h0 ? 1u : 0u;
       checks += act ? (h0 ? 1u : min(dg[k], 2u)) : 0u;  // (a second-neighbour hit implies dg >= 2)
       if (found) par_out[32 * k] = h0 ? hv[k].x : hv[k].y;
       foundm |= (uint32_t)found << k;
@@ -992,6 +1000,10 @@ RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uin
     acc.n += __popc(foundm);
     acc.deg += dsum;
     acc.maxdeg = max(acc.maxdeg, dmax);
+    if (s_p1) {  // partitioned modes: first-neighbour hits (bu_reduced pass 1)
+      const uint32_t c = __reduce_add_sync(RB_FULL, h0m);
+      if (lane == 0 && c) atomicAdd(s_p1, c);
+    }
     // Longer rows that did not hit: the (lane, k) pairs are compacted across
     // the warp through shared memory so every lane continues one row (up to
     // kK2 checks, 4 per step); rows longer still are finished by the whole warp.
@@ -1271,6 +1283,84 @@ __device__ __forceinline__ void block_add3(unsigned long long* red, const Acc& a
 
 
 // ---------------------------------------------------------------------------
+// Partition live bounds (partition.py:143-171 shrink_bounds, applied by
+// bu_reduced before and after each pass; the bounds persist within a
+// traversal).  Shrinking is monotone in the visited set, so the bounds after
+// a bottom-up level equal one shrink of the partition's full range against
+// the visited bitmap after the level: lo = the first 512-vertex block that is
+// not all visited, hi = the end of the last one (aligned ends; the final,
+// unaligned end stays).  Blocks past n_dev are isolated (premarked visited)
+// and the block holding the reference bitmap's padding (n_full % 512 != 0)
+// is never full; both are settled in live_total.
+
+__device__ void live_pass(const KParams& p) {
+  const uint32_t lane = rb::lane_id();
+  const int64_t nb = (p.n_dev + 511) / 512;
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  for (uint64_t b0 = (uint64_t)blockIdx.x * kThreads + (threadIdx.x & ~31u); b0 < (uint64_t)nb; b0 += stride) {
+    const int64_t b = (int64_t)(b0 + lane);
+    bool nonfull = false;
+    if (b < nb) {
+      const uint4* w = reinterpret_cast<const uint4*>(p.vis + b * 16);
+      const uint4 a = __ldcg(w), c = __ldcg(w + 1), d = __ldcg(w + 2), e = __ldcg(w + 3);
+      nonfull = (a.x & a.y & a.z & a.w & c.x & c.y & c.z & c.w & d.x & d.y & d.z & d.w & e.x & e.y & e.z & e.w) !=
+                0xffffffffu;
+    }
+    // partition of block b: last bound <= b (bounds ascending, n_parts small)
+    int32_t part = -1;
+    if (nonfull) {
+      int32_t lo = 0, hi = (int32_t)p.n_parts;  // part_blk[lo] <= b < part_blk[hi]
+      while (hi - lo > 1) {
+        const int32_t mid = (lo + hi) >> 1;
+        if (__ldg(p.part_blk + mid) <= b) lo = mid; else hi = mid;
+      }
+      part = lo;
+    }
+    const uint32_t m = __ballot_sync(RB_FULL, nonfull);
+    if (!m) continue;
+    const int32_t p0 = __shfl_sync(RB_FULL, part, __ffs(m) - 1);
+    if (__all_sync(RB_FULL, !nonfull || part == p0)) {  // one partition: one min / max per warp
+      if ((int)lane == __ffs(m) - 1) atomicMin(p.part_first + p0, (int32_t)b);
+      if ((int)lane == 31 - __clz(m)) atomicMax(p.part_last + p0, (int32_t)b);
+    } else if (nonfull) {
+      atomicMin(p.part_first + part, (int32_t)b);
+      atomicMax(p.part_last + part, (int32_t)b);
+    }
+  }
+}
+
+// One warp (CTA 0): sum of the shrunk partition sizes; re-arms first / last.
+__device__ void live_total(const KParams& p, long long* s_out) {
+  const uint32_t lane = rb::lane_id();
+  const int64_t tail = (p.n_full % 512) ? (p.n_full - 1) / 512 : -1;  // never-full padding block
+  const int64_t nb_dev = (p.n_dev + 511) / 512;
+  long long sum = 0;
+  for (int64_t q = lane; q < p.n_parts; q += 32) {
+    const int64_t b0 = p.part_blk[q], b1 = p.part_blk[q + 1];
+    int64_t f = __ldcg(p.part_first + q), l = __ldcg(p.part_last + q);
+    if (f == INT32_MAX) f = INT64_MAX;
+    // blocks [nb_dev, b1) hold only isolated vertices (full); the block with the
+    // reference bitmap's zero padding is never full, wherever n_dev ends
+    (void)nb_dev;
+    if (tail >= b0 && tail < b1) {
+      f = min(f, tail);
+      l = max(l, tail);
+    }
+    const bool last = q == p.n_parts - 1;
+    const int64_t end = last ? p.n_full : b1 * 512;
+    if (end % 512 == 0)
+      sum += (l >= 0) ? (l + 1 - f) * 512 : 0;
+    else
+      sum += end - f * 512;  // the unaligned final end never moves (and its block is never full)
+    p.part_first[q] = INT32_MAX;
+    p.part_last[q] = -1;
+  }
+  sum = (long long)rb::warp_sum_u64((unsigned long long)sum);
+  if (lane == 0) *s_out = sum;
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------------------
 // Solo levels: the first top-down levels of a traversal usually hold a
 // handful of rows (the source, then its neighbours).  A whole-grid level
 // costs a full pass of scans plus a grid barrier (~7 us); CTA 0 instead runs
@@ -1419,6 +1509,10 @@ __device__ __forceinline__ void solo_levels(const KParams& p, uint32_t* smem, So
       r.n_next = n_next;
       r.t_queue_ns = 0;
       r.reserved = 0;  // executed direction (solo levels: top-down)
+      r.pass1_hits = -1;
+      r.live_vertices = -1;
+      r.claimed = -1;
+      r.reserved2 = 0;
       p.rec[done] = r;
       t_prev = t_now;
     }
@@ -1452,7 +1546,9 @@ __device__ __forceinline__ void solo_levels(const KParams& p, uint32_t* smem, So
   }
 }
 
-template <bool kRev, int KB>
+// kPart: the partitioned modes' record fields (pass-1 hits, live bounds);
+// a separate instantiation so the fast kernels carry none of that code.
+template <bool kRev, int KB, bool kPart>
 __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
   // Sparse bottom-up lists only in the large-graph build (8-word steps): at
   // scale 22 the tail levels are latency floors either way and the extra
@@ -1465,6 +1561,8 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
   __shared__ uint32_t s_bu_next[2];  // bottom-up: next step of this CTA (level parity)
   __shared__ SoloShared s_solo;
   __shared__ uint32_t s_wtot[32];
+  __shared__ uint32_t s_p1;          // first-neighbour hits of this CTA in the current bottom-up level
+  __shared__ long long s_live;       // live_vertices of the current level (CTA 0)
   if (p.dbg && threadIdx.x == 0 && blockIdx.x == 0) p.dbg[kDbgPhase + 63 * 8 + 0] = globaltimer();  // kernel entry
   __shared__ long long s_mf0;  // deg(src) at a traversal start (one load per CTA, not per thread)
   if (threadIdx.x == 0) {
@@ -1559,6 +1657,7 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
     if (blockIdx.x == 0 && threadIdx.x < sizeof(Slot) / 8)
       reinterpret_cast<unsigned long long*>(p.slots + r1)[threadIdx.x] = 0ull;
     if (threadIdx.x == 0) s_bu_next[(L + 1) & 1] = 0u;  // the next level's counter (idle during this one)
+    if (threadIdx.x == 0) s_p1 = 0u;  // (read after this level's block reduction, a __syncthreads later)
 
     // Execution direction.  The level keeps the reference policy's label
     // (records, next decisions); the work is done the cheaper way.  Same next
@@ -1650,14 +1749,15 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
       } else if (kSparseOK && collect) {  // bitmap pass that also lists the vertices left unvisited
         if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&out->ul_count, 1ull << 40);
         bu_level<kRev, KB, true>(p, L, fcur, fnext, nz_of(p, r1), acc, s_bu_found[wib], s_bu_pair[wib],
-                                 &s_bu_next[L & 1], lout, &out->ul_count);
+                                 &s_bu_next[L & 1], lout, &out->ul_count, nullptr);
       } else
         bu_level<kRev, KB, false>(p, L, fcur, fnext, nz_of(p, r1), acc, s_bu_found[wib], s_bu_pair[wib],
-                                  &s_bu_next[L & 1], nullptr, nullptr);
+                                  &s_bu_next[L & 1], nullptr, nullptr, (kPart && p.count_p1) ? &s_p1 : nullptr);
     }
     if (p.dbg && (threadIdx.x & 31) == 0 && done < 64)  // RB_DEBUG_TS: per-warp end of work
       p.dbg[kDbgWarpBase + ((uint64_t)done * gridDim.x + blockIdx.x) * kWarps + (threadIdx.x >> 5)] = globaltimer();
-    block_add3(s_red, acc, out);
+    block_add3(s_red, acc, out);  // (its __syncthreads also orders the CTA's s_p1 updates)
+    if (kPart && p.count_p1 && threadIdx.x == 0 && s_p1) atomicAdd(&out->pad3, (unsigned long long)s_p1);
     const uint64_t tB = globaltimer();
     {
       if constexpr (kSparseOK) {
@@ -1680,6 +1780,11 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
     const int64_t n_next = (int64_t)s_ctr[0];
     const int64_t deg_next = (int64_t)s_ctr[1];
     hubs = s_ctr[2] > kLightDeg;
+    if (kPart && p.n_parts > 0 && xdir == 1) {  // PartitionSet.live_total() after this bottom-up level
+      live_pass(p);
+      rb::grid_barrier(p.bar, nblocks, epoch);
+      if (blockIdx.x == 0 && (threadIdx.x >> 5) == 1) live_total(p, &s_live);
+    }
     if (p.dbg && threadIdx.x == 0 && done < 64) p.dbg[((uint64_t)done * gridDim.x + blockIdx.x) * 4 + 3] = globaltimer() + (uint64_t)(n_next & 0) + (uint64_t)(deg_next & 0) + (hubs ? 0 : 0);
     if (blockIdx.x == 0 && threadIdx.x == 32) {
       const uint64_t t_now = globaltimer();
@@ -1694,6 +1799,10 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
       r.n_next = n_next;
       r.t_queue_ns = (int64_t)t_queue;
       r.reserved = xdir;  // executed direction
+      r.pass1_hits = (kPart && p.count_p1 && xdir == 1) ? (int64_t)rb::ld_relaxed_u64(&out->pad3) : -1;
+      r.live_vertices = (kPart && p.n_parts > 0 && xdir == 1) ? (int64_t)s_live : -1;
+      r.claimed = -1;
+      r.reserved2 = 0;
       p.rec[done] = r;
       t_queue = 0;
       t_prev = t_now;
@@ -1866,14 +1975,19 @@ struct rb_bfs {
   int64_t probe_mf;
   int64_t defer_mf;
   void* stream;
+  bool exact;            // RB_PART_EXACT: run the labelled direction every level
+  int32_t* part_dev;     // [n_parts + 1 block bounds | first | last]
 };
 
 // The traversal kernel of an engine: scan direction x bottom-up step width.
 static const void* bfs_kernel(const rb_bfs* h) {
   bool small = h->n_dev <= kSmallGraph;
   if (const char* env = getenv("RB_KB")) small = atoi(env) == 4;  // tuning override
-  if (h->bu_reverse) return small ? (const void*)bfs_persistent<true, 4> : (const void*)bfs_persistent<true, 8>;
-  return small ? (const void*)bfs_persistent<false, 4> : (const void*)bfs_persistent<false, 8>;
+  if (h->bu_reverse)
+    return small ? (const void*)bfs_persistent<true, 4, false> : (const void*)bfs_persistent<true, 8, false>;
+  if (h->kp.count_p1 || h->kp.n_parts)  // partitioned modes: pass-1 hits / live bounds in the records
+    return small ? (const void*)bfs_persistent<false, 4, true> : (const void*)bfs_persistent<false, 8, true>;
+  return small ? (const void*)bfs_persistent<false, 4, false> : (const void*)bfs_persistent<false, 8, false>;
 }
 
 // RB_ERR_ARG with a message for a null handle / argument (every ARG path sets the error text)
@@ -2060,7 +2174,8 @@ extern "C" int rb_bfs_destroy(rb_bfs* h) {
   if (!h) return RB_OK;
   KParams& k = h->kp;
   void* ptrs[] = {k.vis, k.fb0, k.fb1, k.fb2, h->vis_template, h->pad_mask, k.hq0, k.hq1, k.hs0, k.hs1, k.ul0, k.ul1, k.solo_q, k.parent,
-                  k.level, k.slots, k.bar, k.rec, k.fin, k.nz0, k.nz1, k.nz2, h->hot, h->vinfo, k.dbg, h->td_vinfo};
+                  k.level, k.slots, k.bar, k.rec, k.fin, k.nz0, k.nz1, k.nz2, h->hot, h->vinfo, k.dbg, h->td_vinfo,
+                  h->part_dev};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (h->ev_start) cudaEventDestroy(h->ev_start);
@@ -2068,6 +2183,53 @@ extern "C" int rb_bfs_destroy(rb_bfs* h) {
     if (h->ev_chunk[i]) cudaEventDestroy(h->ev_chunk[i]);
   if (h->ev_end) cudaEventDestroy(h->ev_end);
   delete h;
+  return RB_OK;
+}
+
+__global__ void part_init(int32_t* first, int32_t* last, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    first[i] = INT32_MAX;
+    last[i] = -1;
+  }
+}
+
+extern "C" int rb_bfs_set_partitions(rb_bfs* h, const int64_t* h_bounds, int64_t n_parts, int64_t n_full,
+                                     int32_t flags) {
+  if (!h || n_parts < 0 || (n_parts > 0 && !h_bounds) || n_full < h->n_dev) {
+    rb_set_error("rb_bfs_set_partitions: invalid argument");
+    return RB_ERR_ARG;
+  }
+  KParams& k = h->kp;
+  if (h->part_dev) cudaFree(h->part_dev);
+  h->part_dev = nullptr;
+  k.n_parts = 0;
+  k.part_blk = nullptr;
+  k.part_first = k.part_last = nullptr;
+  h->exact = (flags & RB_PART_EXACT) != 0;
+  k.count_p1 = (flags & RB_PART_COUNT_PASS1) ? 1 : 0;
+  k.n_full = n_full;
+  if (n_parts == 0 || !(flags & RB_PART_SHRINK)) return RB_OK;
+  std::vector<int32_t> blk((size_t)n_parts + 1);
+  int64_t prev = 0;
+  for (int64_t i = 0; i <= n_parts; ++i) {
+    const int64_t b = i < n_parts ? h_bounds[i] : n_full;
+    const bool bad = (i < n_parts && b % 512) || b < prev || b > n_full || (i == 0 && b != 0);
+    prev = b;
+    if (bad) {
+      rb_set_error("rb_bfs_set_partitions: partition starts must ascend and be 512-aligned");
+      return RB_ERR_ARG;
+    }
+    blk[(size_t)i] = (int32_t)((b + 511) / 512);
+  }
+  int rc = alloc_dev((void**)&h->part_dev, (size_t)(3 * n_parts + 1) * sizeof(int32_t));
+  if (rc) return rc;
+  RB_CUDA_TRY(cudaMemcpy(h->part_dev, blk.data(), blk.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  k.part_blk = h->part_dev;
+  k.part_first = h->part_dev + n_parts + 1;
+  k.part_last = k.part_first + n_parts;
+  part_init<<<64, 256>>>(k.part_first, k.part_last, n_parts);
+  RB_CUDA_TRY(cudaDeviceSynchronize());
+  k.n_parts = n_parts;
   return RB_OK;
 }
 
@@ -2126,7 +2288,7 @@ static int launch(rb_bfs* h, cudaStream_t s, int64_t level0, int64_t dir0, int64
   kp.from_fin = from_fin;
   // the cost-model execution (a level may run the other way) only in hybrid
   // modes: level_sync / sequential are top-down only (engine.py use_dir)
-  kp.exec_opt = (exec && h->exec_opt && h->prm.hybrid) ? 1 : 0;
+  kp.exec_opt = (exec && h->exec_opt && h->prm.hybrid && !h->exact) ? 1 : 0;
   kp.reached0 = reached0;
   kp.probe_mf = h->probe_mf;
   kp.defer_mf = h->defer_mf;

@@ -11,12 +11,17 @@ traversal runs on the device through the C ABI (include/rcmbfs_b200.h):
 * Isolated vertices beyond the last non-isolated id are dropped from the
   device state (after RCM they are the tail [|V+|, n)); isolated vertices
   inside the range are premarked visited (engine.py:432-437).
-* Modes: ``hybrid`` / ``hybrid_balanced`` scan bottom-up rows from their end
-  (RCM ids ascend with degree); ``hybrid_reduced`` scans the descending-degree
-  adjacency ``g_desc`` forward (Alg. 6 order); ``level_sync`` and
-  ``sequential`` are top-down only.  Parents may differ from the CPU
-  reference's (any valid BFS tree); levels, per-level n_f / m_f / m_u and
-  directions are identical.
+* Modes: ``hybrid`` (the fast path) scans bottom-up rows from their end (RCM
+  ids ascend with degree) and executes each level the cheaper way, keeping
+  the policy's labels; its levels, directions and n_f / m_f / m_u equal the
+  reference's.  The paper's modes run every level as labelled and scan in
+  the reference's order -- ``hybrid_balanced`` the ascending rows (bu_steal),
+  ``hybrid_reduced`` the descending-degree adjacency ``g_desc`` (Alg. 6
+  bu_reduced) -- so their LevelRecords match the reference field for field:
+  scanned_edges, pass1_hits, live_vertices (partition.py shrink rule over
+  get_partitions(n, partition_factor, threads)) and claimed.  ``level_sync``
+  and ``sequential`` are top-down only.  Parents may differ from the CPU
+  reference's (any valid BFS tree).
 
 There is no CPU fallback: constructing an engine without CUDA raises.
 """
@@ -48,6 +53,7 @@ __all__ = [
 TOP_DOWN = "top_down"
 BOTTOM_UP = "bottom_up"
 MODES = ("sequential", "level_sync", "hybrid", "hybrid_balanced", "hybrid_reduced")
+_PARTITIONED_MODES = ("hybrid_balanced", "hybrid_reduced")
 
 
 def default_partition_factor(n: int) -> int:
@@ -427,15 +433,25 @@ def fresh_int32(n: int) -> np.ndarray:
     return np.frombuffer(h, dtype=np.int32)
 
 
-def _records_to_levels(recs) -> list:
+def _records_to_levels(recs, part=None) -> list:
+    """Device records -> LevelRecords.  ``part`` = (n_partitions, live_fixed):
+    the partitioned modes' bottom-up levels report ``claimed`` = every
+    partition (each is claimed once per step, _kernels.py:176-293) and, for
+    hybrid_balanced (bounds never shrink), ``live_vertices`` = live_fixed."""
     out = []
     for r in recs:
+        bu = r.direction != 0
+        claimed = part[0] if (part is not None and bu) else None
+        live = int(r.live_vertices) if r.live_vertices >= 0 else None
+        if part is not None and bu and part[1] is not None:
+            live = part[1]
         out.append(
             LevelRecord(
                 level=int(r.level), direction=TOP_DOWN if r.direction == 0 else BOTTOM_UP, n_f=int(r.n_f),
                 m_f=int(r.m_f), m_u=int(r.m_u), scanned_edges=int(r.scanned_edges), wall_time=r.t_ns * 1e-9,
                 per_thread_edges=np.array([int(r.scanned_edges)], dtype=np.int64), queue_time=r.t_queue_ns * 1e-9,
                 executed_direction=TOP_DOWN if r.reserved == 0 else BOTTOM_UP,
+                pass1_hits=int(r.pass1_hits) if r.pass1_hits >= 0 else None, live_vertices=live, claimed=claimed,
             )
         )
     return out
@@ -464,10 +480,29 @@ class BfsEngine:
         self.pool = None  # device engine: no host worker pool
         hybrid = params.mode not in ("sequential", "level_sync")
         reduced = params.mode == "hybrid_reduced"
+        partitioned = params.mode in _PARTITIONED_MODES
+        # hybrid: bottom-up rows scanned from their end (RCM ids ascend with
+        # degree) and each level executed the cheaper way.  The paper's modes
+        # run exactly as labelled and scan in the reference's order (ascending
+        # rows for hybrid_balanced, the descending-degree adjacency for
+        # hybrid_reduced), so every LevelRecord field equals the reference's.
         self._dev = _DeviceBfs(
             g, hybrid=hybrid, alpha=params.alpha, beta=params.beta, g_bu=g_desc if reduced else None,
-            bu_reverse=not reduced, trim_isolated=True, record_levels=record_levels,
+            bu_reverse=not partitioned, trim_isolated=True, record_levels=record_levels,
         )
+        self._part = None
+        if partitioned and g.n >= 1:
+            from .partition import get_partitions
+
+            self.ps = get_partitions(g.n, params.partition_factor, params.threads)  # engine.py:499-500
+            flags = _lib.RB_PART_EXACT
+            if reduced:
+                flags |= _lib.RB_PART_COUNT_PASS1 | _lib.RB_PART_SHRINK
+            if self._dev.h:
+                st = np.ascontiguousarray(self.ps.starts, dtype=np.int64)
+                _lib.check(_lib.lib().rb_bfs_set_partitions(self._dev.h, st.ctypes.data_as(ctypes.c_void_p),
+                                                            st.size, g.n, flags), "rb_bfs_set_partitions")
+            self._part = (self.ps.n_partitions, None if reduced else g.n)
         self._deg_host = g.degrees  # host copy (once per graph): the per-run isolated-source check
 
     @property
@@ -501,7 +536,7 @@ class BfsEngine:
         if source >= self._dev.n_dev or int(self._deg_host[source]) == 0:
             return self._trivial(source)
         pred, recs, elapsed = self._dev.run_to_host(source, g.n)
-        levels = _records_to_levels(recs)
+        levels = _records_to_levels(recs, self._part)
         traversed = sum(r.m_f for r in levels) // 2  # = sum deg[reached] // 2 (engine.py:599-600)
         return BfsResult(source=source, n=g.n, predecessor=pred, levels=levels, elapsed_time=elapsed,
                          traversed_edges=traversed, mode=self.params.mode)
@@ -513,7 +548,7 @@ class BfsEngine:
         tensor of n_dev) is given, the level array is copied into it."""
         self._dev.traverse(int(source))
         recs, elapsed = self._dev.results(want_parent=False, level_out=levels_out)
-        return elapsed, _records_to_levels(recs)
+        return elapsed, _records_to_levels(recs, self._part)
 
     def parent_device(self):
         """int32 CUDA tensor view of the engine's parent array [0, n_dev)."""

@@ -5,6 +5,8 @@ Graphs here are built by the (pinned) oracle and uploaded, so these tests
 isolate the traversal kernels; tests/test_gpu_prep.py covers the device
 preprocessing and the full pipeline."""
 
+import warnings
+
 import numpy as np
 import pytest
 
@@ -297,3 +299,62 @@ def test_engine_knobs_keep_parity(cuda_ok, ocache, monkeypatch, knobs):
                 assert np.array_equal(lev.astype(np.int32), want), (knobs, scale, s)
                 got = [(0 if r.direction == rb.TOP_DOWN else 1, r.n_f, r.m_f, r.m_u) for r in res.levels]
                 assert got == [tuple(int(x) for x in r[1:5]) for r in rec], (knobs, scale, s)
+
+
+# ---------------------------------------------------------------------------
+# the paper's partitioned modes: every LevelRecord field vs the reference
+
+
+def test_partitioned_modes_match_reference_records(cuda_ok, golden_modes, ocache):
+    from conftest import mode_records
+
+    for key, cases in golden_modes.items():
+        scale, seed = map(int, key.split(","))
+        g2 = ocache.kron(scale, seed)["g2"]
+        labels = oracle.csr_components(g2)
+        g, gd = to_rb(g2), desc_of(g2)
+        engines = {}
+        try:
+            for c in cases:
+                k = (c["mode"], c["threads"], c["partition_factor"])
+                if k not in engines:
+                    with warnings.catch_warnings():
+                        warnings.simplefilter("ignore")
+                        engines[k] = rb.BfsEngine(g, rb.BfsParams(mode=c["mode"], threads=c["threads"],
+                                                                  partition_factor=c["partition_factor"]),
+                                                  g_desc=gd)
+                res = engines[k].run(c["source"])
+                assert mode_records(res.levels, False) == c["records"], (key, k, c["source"])
+                check_run(g2, labels, res, c["source"])
+        finally:
+            for e in engines.values():
+                e.close()
+
+
+def test_reduced_mode_records_vs_oracle_random_graphs(cuda_ok):
+    """live_vertices edge cases: isolated vertices inside the range and in
+    the tail, n not a multiple of 512, single-block partitions."""
+    from conftest import mode_records
+
+    rng = np.random.default_rng(77)
+    for it in range(16):
+        n = int(rng.integers(300, 9000))
+        m = int(n * rng.uniform(0.4, 3.0))
+        e = rng.integers(0, n, size=(m, 2), dtype=np.uint32)
+        g_or = oracle.build_csr(n, e)
+        if it % 2:  # RCM graph: isolated tail dropped on device
+            g_or = oracle.apply_permutation(g_or, oracle.rcm(g_or)[0])
+        gd = oracle.degree_sort_rows(g_or, True)
+        labels = oracle.csr_components(g_or)
+        threads, lam = int(rng.integers(1, 5)), int(rng.integers(1, 12))
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            eng = rb.BfsEngine(to_rb(g_or), rb.BfsParams(mode="hybrid_reduced", threads=threads, partition_factor=lam),
+                               g_desc=rb.CsrGraph(n, g_or.row_starts, gd, g_or.degrees))
+        with eng:
+            for s in rng.choice(np.flatnonzero(g_or.degrees > 0), size=4, replace=False):
+                _, _, rec, _ = oracle.bfs_run(g_or, int(s), "hybrid_reduced", threads=threads, partition_factor=lam,
+                                              g_desc_dst=gd)
+                res = eng.run(int(s))
+                assert mode_records(res.levels, False) == mode_records(rec, True), (it, int(s))
+                check_run(g_or, labels, res, int(s))
