@@ -1,24 +1,34 @@
 #!/usr/bin/env python
-"""Benchmark: BFS GTEPS (harmonic mean over seeded roots) on the RCM-reordered
-Kronecker graph of BASELINE.json configs[1] (scale 22, edgefactor 16).
+"""Benchmark: BFS GTEPS (harmonic mean over the 64 seeded roots) on the
+RCM-reordered Kronecker graph of BASELINE.json configs[2] (scale 26,
+edgefactor 16) -- the largest configuration that fits one B200.
 
-A "step" is one BFS traversal from one seeded root (the reference's
-BfsEngine.run, engine.py:518-604) over the HBM-resident RCM graph.  The
-headline per-root TEPS numerator is the raw input pairs in the root's
-component (bench.py:186-189, 336-338 of the reference; the paper's
-convention); the dedup numerator (traversed edges) is reported alongside.
+A "step" is one sweep of the 64 seeded roots (reference bench.py:124-134),
+each root one BFS (BfsEngine.run, engine.py:518-604) over the HBM-resident
+RCM graph with the L2 flushed before it.  Per-root time = the mean of that
+root's device traversal time over the K timed sweeps; the headline per-root
+TEPS numerator is the raw input pairs in the root's component (reference
+bench.py:186-189, 336-338; the paper's / north star's convention), the dedup
+numerator (traversed edges, engine.py:599-600) is reported alongside; value =
+harmonic mean over the 64 roots (bench.py:235-237).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--scale S] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--scale S] [--graph kronecker|chunglu]
+                  [--impl ours|reference] [--replicas]
 
 Rank 0 prints ONE JSON line.  ``--impl reference`` times the CPU reference
-path (the oracle port of BfsEngine hybrid mode, C + OpenMP on all host
-cores) on the same config -- it never touches the CUDA library.
+path (the oracle's C + OpenMP port of BfsEngine, modes hybrid_reduced -- the
+paper's full method -- and hybrid, on all host cores) on the same config; it
+never loads the CUDA library.  ``--gpus N`` (torchrun): the 1D vertex-block
+partition (one traversal per root over all GPUs, strong scaling);
+``--replicas`` instead shards the 64 roots over per-GPU graph replicas
+(throughput mode, labelled as such).
 """
 
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -32,32 +42,34 @@ sys.path.insert(0, ROOT)
 
 METRIC = "BFS GTEPS (harmonic mean, 64 roots) on RCM-reordered Kronecker graphs"
 UNIT = "GTEPS"
+N_ROOTS = 64
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=64)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=5, help="timed sweeps of the 64 roots")
+    ap.add_argument("--warmup", type=int, default=3, help="untimed sweeps (W >= 3)")
     ap.add_argument("--graph", default="kronecker", choices=["kronecker", "chunglu"],
                     help="kronecker (configs[0..3]) or chunglu (configs[4]: n=2^24, gamma 2.1, seed 7)")
-    ap.add_argument("--scale", type=int, default=22)
+    ap.add_argument("--scale", type=int, default=26)
     ap.add_argument("--edgefactor", type=int, default=16)
     ap.add_argument("--seed", type=int, default=None, help="default: 1 (kronecker), 7 (chunglu)")
     ap.add_argument("--mode", default="hybrid")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="cpu_baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--profile-roots", type=int, default=0, help="only run N roots (for ncu)")
-    ap.add_argument("--partitioned", action="store_true",
-                    help="N > 1: ONE traversal per root over the 1D vertex-block partition (NCCL exchange per "
-                         "level; for graphs beyond one GPU).  Default: the 64 independent roots are sharded "
-                         "over the GPUs, each with its own replica of the graph (no data-path collective)")
-    ap.add_argument("--validate-roots", type=int, default=64,
-                    help="validate this many of the timed roots' trees on the GPU (outside the timed region)")
+    ap.add_argument("--profile-roots", type=int, default=0, help="only run N roots once (for ncu)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: shard the 64 independent roots over per-GPU graph replicas (throughput mode). "
+                         "Default: ONE traversal per root over the 1D vertex-block partition of all GPUs")
+    ap.add_argument("--validate-roots", type=int, default=N_ROOTS,
+                    help="validate this many roots' trees on the GPU (outside the timed region)")
     a = ap.parse_args()
     if a.seed is None:
         a.seed = 7 if a.graph == "chunglu" else 1
+    a.warmup = max(a.warmup, 0)
+    a.steps = max(a.steps, 1)
     return a
 
 
@@ -193,10 +205,17 @@ def load_traffic(name: str):
 
 
 # ---------------------------------------------------------------------------
-# CPU reference arm (oracle port of BfsEngine hybrid, all host cores)
+# CPU reference arm (the oracle's C + OpenMP port of BfsEngine, all host cores)
+
+
+def default_partition_factor(n: int) -> int:
+    """engine.py:70-72 (the CPU engine's lambda)."""
+    return 10 if n < (1 << 26) else 20
 
 
 def cpu_graph(args):
+    """The same workload built by the oracle on the host (C + OpenMP restatement
+    of generator.py / graph.py / reorder.py): no CUDA library is loaded."""
     import oracle
 
     t0 = time.perf_counter()
@@ -208,19 +227,23 @@ def cpu_graph(args):
     g = oracle.build_csr(n, e)
     t2 = time.perf_counter()
     perm, n_plus, ranges = oracle.rcm(g)
-    g2 = oracle.apply_permutation(g, perm)
+    del g
     t3 = time.perf_counter()
+    g = oracle.build_csr(n, e)  # (rebuilt: rcm and apply_permutation timed apart, bench.py:160-163)
+    g2 = oracle.apply_permutation(g, perm)
+    del g
+    t4 = time.perf_counter()
     inv = oracle.inverse(perm)
     return dict(n=n, edges=e, g2=g2, perm=perm, inv=inv, n_plus=n_plus, ranges=ranges,
-                timings={"generate_s": t1 - t0, "csr_build_s": t2 - t1, "rcm_s": t3 - t2})
+                timings={"generate_s": t1 - t0, "csr_build_s": t2 - t1, "rcm_s": t3 - t2,
+                         "apply_permutation_s": t4 - t3})
 
 
 def raw_pairs_for(ranges, inv, edges, roots):
     """Raw input pairs whose first endpoint lies in each root's component."""
     starts = np.array([a for a, _ in ranges], np.int64)
     lab_u = inv[edges[:, 0]].astype(np.int64)
-    out = []
-    cache = {}
+    out, cache = [], {}
     for s in roots:
         ci = int(np.searchsorted(starts, s, side="right") - 1)
         if ci not in cache:
@@ -230,24 +253,35 @@ def raw_pairs_for(ranges, inv, edges, roots):
     return np.array(out, np.int64)
 
 
-def cpu_bfs_sample(cg, roots, raw, seconds, threads=0):
-    """Time the oracle hybrid BFS on roots until `seconds` elapse (>=1 root)."""
+def cpu_run(g2, gd, s, mode, threads):
+    """One BfsEngine.run in the oracle port; returns its elapsed_time (the level
+    loop, engine.py:534-598, reset excluded)."""
     import oracle
 
-    g2 = cg["g2"]
-    oracle.hybrid_bfs(g2, int(roots[0]), threads=threads)  # warm-up (reference has none; cold caches hurt)
-    teps, used = [], 0
-    t_start = time.perf_counter()
-    for s, rp in zip(roots, raw):
-        _, rec, el = oracle.hybrid_bfs(g2, int(s), threads=threads)
-        teps.append(rp / el)
-        used += 1
-        if time.perf_counter() - t_start > seconds:
+    lam = default_partition_factor(g2.n)
+    _, _, _, el = oracle.bfs_run(g2, int(s), mode, threads=threads, partition_factor=lam,
+                                 g_desc_dst=gd if mode == "hybrid_reduced" else None)
+    return el
+
+
+def cpu_sample(g2, gd, roots, raw, mode, threads, seconds, max_roots=N_ROOTS):
+    """hmean GTEPS of the port over roots until `seconds` elapse (>= 1 root; one warm-up root first)."""
+    cpu_run(g2, gd, roots[0], mode, threads)
+    teps, t0 = [], time.perf_counter()
+    for s, rp in zip(roots[:max_roots], raw[:max_roots]):
+        teps.append(rp / cpu_run(g2, gd, s, mode, threads))
+        if time.perf_counter() - t0 > seconds:
             break
-    return hmean(teps) / 1e9, used
+    return hmean(teps) / 1e9, len(teps)
 
 
 def run_reference(args):
+    """bench.py --impl reference: the reference's CPU path on this box's host
+    cores, same config / metric / unit as our arm.  Primary = hybrid_reduced
+    (the paper's full method, Alg. 6 over the descending-degree adjacency) at
+    all host threads: each step runs a bounded sample of ceil(64 / K) roots so
+    the K steps cover all 64 seeded roots; value = hmean over the 64 roots.
+    Also sampled: mode hybrid (all threads) and both modes at 1 thread."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -256,36 +290,106 @@ def run_reference(args):
     oracle.build()
     threads = os.cpu_count() or 1
     cg = cpu_graph(args)
-    roots = oracle.sample_sources(cg["g2"].degrees, 64, 1)
-    raw = raw_pairs_for(cg["ranges"], cg["inv"], cg["edges"], roots)
-    for s in roots[: args.warmup]:
-        oracle.hybrid_bfs(cg["g2"], int(s), threads=threads)
-    teps, times = [], []
-    k = min(args.steps, len(roots))
+    g2 = cg["g2"]
     t0 = time.perf_counter()
-    for s, rp in zip(roots[:k], raw[:k]):
-        _, _, el = oracle.hybrid_bfs(cg["g2"], int(s), threads=threads)
-        teps.append(rp / el)
-        times.append(el)
-    wall = time.perf_counter() - t0
+    gd = oracle.degree_sort_rows(g2, True)  # degree_sort_adjacency(g, "descending")
+    t_desc = time.perf_counter() - t0
+    roots = oracle.sample_sources(g2.degrees, N_ROOTS, 1)
+    raw = raw_pairs_for(cg["ranges"], cg["inv"], cg["edges"], roots)
+    del cg["edges"]
+    primary = "hybrid_reduced"
+    rps = -(-N_ROOTS // args.steps)  # roots per step
+    for i in range(args.warmup):
+        for j in range(rps):
+            cpu_run(g2, gd, roots[(i * rps + j) % N_ROOTS], primary, threads)
+    per_root = {}
+    step_wall = []
+    for i in range(args.steps):
+        t0 = time.perf_counter()
+        for j in range(rps):
+            k = (i * rps + j) % N_ROOTS
+            el = cpu_run(g2, gd, roots[k], primary, threads)
+            per_root.setdefault(k, []).append(el)
+        step_wall.append(time.perf_counter() - t0)
+    teps = [raw[k] / float(np.mean(v)) for k, v in sorted(per_root.items())]
     v = hmean(teps) / 1e9
+    modes = {f"{primary}_t{threads}": {"gteps": v, "roots": len(teps)}}
+    b, used = cpu_sample(g2, gd, roots, raw, "hybrid", threads, 20.0, 16)
+    modes[f"hybrid_t{threads}"] = {"gteps": b, "roots": used}
+    for m in (primary, "hybrid"):
+        b, used = cpu_sample(g2, gd, roots, raw, m, 1, 8.0, 4)
+        modes[f"{m}_t1"] = {"gteps": b, "roots": used}
+    sample = (f"{len(teps)} seeded roots ({rps} per step) of the {workload(args)[0]} graph, oracle C port of "
+              f"BfsEngine mode {primary} (td_striped + bu_reduced, lambda {default_partition_factor(g2.n)}), "
+              f"OpenMP {threads} threads; graph built by the oracle on the host")
     line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": k,
-        "warmup": args.warmup, "ms_per_step": 1e3 * wall / k, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "int32", "data": workload(args)[1],
-        "config": {"workload": workload(args)[0], "scale": args.scale,
-                   "edgefactor": args.edgefactor, "roots": k, "mode": "hybrid"},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{k} seeded roots of the {workload(args)[0]} graph, oracle C port of "
-                                   f"BfsEngine hybrid (td_plain + bu_range), OpenMP {threads} threads"},
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(step_wall)), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": workload(args)[1],
+        "config": {"workload": workload(args)[0], "scale": args.scale, "edgefactor": args.edgefactor,
+                   "roots": N_ROOTS, "mode": primary},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "modes": modes,
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "preprocessing_s": cg["timings"],
+        "preprocessing_s": dict(cg["timings"], degree_sort_desc_s=t_desc),
     }
     print(json.dumps(line), flush=True)
 
 
 # ---------------------------------------------------------------------------
 # our arm
+
+
+def build_graph(args, rb, torch):
+    """Device preprocessing of the workload (timed separately, not part of the
+    metric): generator -> build_csr -> rcm + apply_permutation.  Returns the RCM
+    graph, its stats, the 64 roots, their raw-pair numerators and the timings."""
+    # one tiny pass first so module loading is not billed to the timings
+    _w = rb.build_csr(rb.kronecker_generate(rb.KroneckerParams(scale=10), device=True))
+    _p, _ = rb.rcm(_w)
+    rb.apply_permutation(_w, _p)
+    if args.graph == "chunglu":
+        rb.chunglu_generate(rb.ChungLuParams(n=1 << 10), device=True)
+    torch.cuda.synchronize()
+    del _w, _p
+    t0 = time.perf_counter()
+    if args.graph == "chunglu":
+        el = rb.chunglu_generate(rb.ChungLuParams(n=1 << args.scale, seed=args.seed), device=True)
+    else:
+        el = rb.kronecker_generate(rb.KroneckerParams(scale=args.scale, edgefactor=args.edgefactor, seed=args.seed),
+                                   device=True)
+    torch.cuda.synchronize()
+    t_gen = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    g = rb.build_csr(el)
+    torch.cuda.synchronize()
+    t_csr = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    perm, stats = rb.rcm(g)
+    torch.cuda.synchronize()
+    t_rcm = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    g2 = rb.apply_permutation(g, perm)
+    torch.cuda.synchronize()
+    t_app = time.perf_counter() - t0
+    del g
+    deg2 = g2.device_arrays()[2]
+    roots = rb.sample_sources(deg2.cpu().numpy(), N_ROOTS, 1)
+    inv_t = perm.device_arrays()[1]
+    lab = inv_t[el.edges[:, 0].long()].long()
+    starts = np.array([a for a, _ in stats.component_ranges], np.int64)
+    raw_cache, raw = {}, []
+    for s in roots:
+        ci = int(np.searchsorted(starts, s, side="right") - 1)
+        if ci not in raw_cache:
+            a, b = stats.component_ranges[ci]
+            raw_cache[ci] = int(((lab >= a) & (lab < b)).sum().item())
+        raw.append(raw_cache[ci])
+    del lab, el
+    torch.cuda.empty_cache()
+    prep = {"generate": t_gen, "csr_build": t_csr, "rcm": t_rcm, "apply_permutation": t_app,
+            "rcm_plus_relabel": t_rcm + t_app}
+    return g2, stats, roots, np.array(raw, np.int64), prep
 
 
 def run_ours(args):
@@ -309,68 +413,30 @@ def run_ours(args):
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    # ---- preprocessing (timed separately, reported, not part of the metric);
-    # one tiny pass first so module loading is not billed to the timings
-    _w = rb.build_csr(rb.kronecker_generate(rb.KroneckerParams(scale=10), device=True))
-    _p, _ = rb.rcm(_w)
-    rb.apply_permutation(_w, _p)
-    if args.graph == "chunglu":
-        rb.chunglu_generate(rb.ChungLuParams(n=1 << 10), device=True)
-    torch.cuda.synchronize()
-    del _w, _p
-    t0 = time.perf_counter()
-    if args.graph == "chunglu":
-        el = rb.chunglu_generate(rb.ChungLuParams(n=1 << args.scale, seed=args.seed), device=True)
-    else:
-        el = rb.kronecker_generate(rb.KroneckerParams(scale=args.scale, edgefactor=args.edgefactor, seed=args.seed),
-                                   device=True)
-    torch.cuda.synchronize()
-    t_gen = time.perf_counter() - t0
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    g = rb.build_csr(el)
-    torch.cuda.synchronize()
-    t_csr = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    perm, stats = rb.rcm(g)
-    g2 = rb.apply_permutation(g, perm)
-    torch.cuda.synchronize()
-    t_rcm = time.perf_counter() - t0
-    del g
+    g2, stats, roots, raw, prep = build_graph(args, rb, torch)
+    if world > 1 and not args.replicas:
+        return run_partitioned(args, rb, torch, dist, g2, stats, roots, raw, world, rank, prep)
 
-    # roots (bench.py:124-134) and raw pairs per root component
-    deg2 = g2.device_arrays()[2]
-    roots = rb.sample_sources(deg2.cpu().numpy(), 64, 1)
-    inv_t = perm.device_arrays()[1]
-    lab = inv_t[el.edges[:, 0].long()].long()
-    starts = np.array([a for a, _ in stats.component_ranges], np.int64)
-    raw_cache, raw = {}, []
-    for s in roots:
-        ci = int(np.searchsorted(starts, s, side="right") - 1)
-        if ci not in raw_cache:
-            a, b = stats.component_ranges[ci]
-            raw_cache[ci] = int(((lab >= a) & (lab < b)).sum().item())
-        raw.append(raw_cache[ci])
-    raw = np.array(raw, np.int64)
-    del lab, el
-
-    if world > 1 and args.partitioned:
-        return run_partitioned(args, rb, torch, dist, g2, stats, roots, raw, world, rank,
-                               {"generate": t_gen, "csr_build": t_csr, "rcm_plus_relabel": t_rcm})
     eng = rb.BfsEngine(g2, rb.BfsParams(mode=args.mode))
     n_dev = eng.n_dev
     n_plus_dev = stats.n_non_isolated
-    # this rank's roots (replicas: roots are dealt round-robin over ranks)
-    order = np.arange(64)
-    k = args.steps if args.profile_roots == 0 else args.profile_roots
-    my = [order[(rank + world * i) % 64] for i in range(k)]
+    # this rank's roots: all 64 on one GPU; replicas take every world-th root
+    my = list(range(rank, N_ROOTS, world))
+    if args.profile_roots:
+        my = my[: args.profile_roots]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    sweeps = 1 if args.profile_roots else args.steps
 
-    for i in range(args.warmup if args.profile_roots == 0 else 1):
-        eng.run_device(int(roots[my[i % len(my)]]))
+    for _ in range(args.warmup if not args.profile_roots else 0):
+        for j in my:
+            flush.zero_()
+            eng.run_device(int(roots[j]))
+    if args.profile_roots:
+        eng.run_device(int(roots[my[0]]))  # one warm-up root before the profiled one
     torch.cuda.synchronize()
 
-    times, teps, teps_dedup, bytes_alg, lvl_counts, per_root = [], [], [], [], [], []
+    t_root = {j: [] for j in my}
+    levels_of = {}
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
@@ -378,31 +444,33 @@ def run_ours(args):
     ev_b = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         ev_a.record()
-        for j in my:
-            flush.zero_()
-            el_s, levels = eng.run_device(int(roots[j]))
-            times.append(el_s)
-            teps.append(raw[j] / el_s)
-            teps_dedup.append((sum(r.m_f for r in levels) // 2) / el_s)
-            per_root.append(level_bytes(levels, n_dev, n_plus_dev))
-            bytes_alg.append(sum(b for _, b, _ in per_root[-1]))
-            lvl_counts.append(len(levels))
+        for _ in range(sweeps):
+            for j in my:
+                flush.zero_()
+                el_s, levels = eng.run_device(int(roots[j]))
+                t_root[j].append(el_s)
+                levels_of[j] = levels
         ev_b.record()
         torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
     wall_ms = ev_a.elapsed_time(ev_b)
 
-    # ---- e2e through the public API: BfsEngine.run -> host predecessor array
-    e2e_teps = []
-    for j in my[:3]:  # warm the host path (pinned staging buffers, result-array pool of the allocator)
+    mean_t = {j: float(np.mean(v)) for j, v in t_root.items()}
+    teps = {j: raw[j] / mean_t[j] for j in my}
+    teps_dedup = {j: (sum(r.m_f for r in levels_of[j]) // 2) / mean_t[j] for j in my}
+    per_root = [level_bytes(levels_of[j], n_dev, n_plus_dev) for j in my]
+    bytes_alg = [sum(b for _, b, _ in lv) for lv in per_root]
+
+    # ---- e2e through the public API: BfsEngine.run -> BfsResult with the host predecessor
+    for j in my[:3]:  # warm the host path (pinned staging buffers, result-array pool)
         eng.run(int(roots[j]))
-    for j in my:  # every timed root (the hmean is sensitive to host-side outliers)
+    e2e_t = {}
+    for j in my:
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         res = eng.run(int(roots[j]))
-        dt = time.perf_counter() - t0
-        e2e_teps.append(raw[j] / dt)
+        e2e_t[j] = time.perf_counter() - t0
     d2h = 4 * n_dev + 64 * len(res.levels)
 
     # ---- tree validation on the GPU (validate.py rules), outside the timed region
@@ -418,70 +486,83 @@ def run_ours(args):
             n_ok += int((bad < 0).all())
         del val, full
 
-    value_rank = hmean(teps) / 1e9
-    ms_rank = 1e3 * float(np.mean(times))
+    # ---- one harmonic mean over all 64 roots (replicas: gathered from every rank)
+    loc = np.zeros((N_ROOTS, 5), np.float64)
+    for j in my:
+        loc[j] = [1.0, teps[j], teps_dedup[j], raw[j] / e2e_t[j], mean_t[j]]
     if dist is not None:
-        t = torch.tensor([value_rank, ms_rank, hmean(e2e_teps) / 1e9], device="cuda", dtype=torch.float64)
-        vals = [torch.zeros_like(t) for _ in range(world)]
-        dist.all_gather(vals, t)
-        vals = torch.stack(vals).cpu().numpy()
-        value = float(vals[:, 0].sum())  # replicas: aggregate traversal throughput
-        ms = float(vals[:, 1].max())
-        e2e_v = float(vals[:, 2].sum())
-    else:
-        value, ms, e2e_v = value_rank, ms_rank, hmean(e2e_teps) / 1e9
-
+        tt = torch.from_numpy(loc).to("cuda" if not one_gpu else "cpu")
+        dist.all_reduce(tt)
+        loc = tt.cpu().numpy()
+        mx = torch.tensor([wall_ms], dtype=torch.float64, device=tt.device)
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        wall_ms = float(mx.item())
+    got = loc[:, 0] > 0
+    value = hmean(loc[got, 1]) / 1e9
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
         return
-
+    sweep_ms = 1e3 * float(loc[got, 4].sum()) / max(world, 1)  # device traversal time of one sweep (per GPU)
     peak, peak_kind = measured_peak()
-    ach = float(np.sum(bytes_alg) / np.sum(times) / 1e9)
+    ach = float(np.sum(bytes_alg) / np.sum([mean_t[j] for j in my]) / 1e9)
     traffic = load_traffic(workload(args)[0])
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": len(my), "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
-        "data": workload(args)[1] + ", built on device",
-        "config": {"workload": workload(args)[0], "scale": args.scale,
-                   "edgefactor": args.edgefactor, "roots": len(my), "mode": args.mode,
-                   "parallelism": "replicas" if world > 1 else "single",
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": sweeps, "warmup": args.warmup,
+        "ms_per_step": sweep_ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "int32", "data": workload(args)[1] + ", built on device",
+        "config": {"workload": workload(args)[0], "scale": args.scale, "edgefactor": args.edgefactor,
+                   "roots": int(got.sum()), "step": f"one sweep of the {N_ROOTS} seeded roots",
+                   "mode": args.mode,
+                   "parallelism": f"replicas x{world} (roots sharded; throughput mode)" if world > 1 else "single",
                    "l2": "flushed (256 MiB write) before every root", "n": int(g2.n), "n_plus": int(n_plus_dev),
                    "m_directed": int(g2.m_directed)},
-        "gteps_dedup_hmean": hmean(teps_dedup) / 1e9,
-        "gteps_min": float(np.min(teps)) / 1e9, "gteps_max": float(np.max(teps)) / 1e9,
-        "depth_median": float(np.median(lvl_counts)) - 1,
-        "preprocessing_s": {"generate": t_gen, "csr_build": t_csr, "rcm_plus_relabel": t_rcm},
+        "gteps_dedup_hmean": hmean(loc[got, 2]) / 1e9,
+        "gteps_min": float(loc[got, 1].min()) / 1e9, "gteps_max": float(loc[got, 1].max()) / 1e9,
+        "ms_per_root_mean": 1e3 * float(loc[got, 4].mean()),
+        "depth_median": float(np.median([len(levels_of[j]) for j in my])) - 1,
+        "preprocessing_s": prep,
         "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                      "peak_kind": peak_kind, "kernel": "bfs_persistent",
                      "bytes_per_launch": float(np.mean(bytes_alg)),
-                     "launch_ms": 1e3 * float(np.mean(times)),
+                     "launch_ms": 1e3 * float(np.mean([mean_t[j] for j in my])),
                      "traffic": None if traffic is None else traffic.get("bytes_per_launch"),
                      "by_direction": by_direction(per_root, peak)},
-        "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": 8, "d2h_bytes_per_step": int(d2h),
-                "api": "BfsEngine.run(source) -> BfsResult with host predecessor"},
+        "e2e": {"value": hmean(loc[got, 3]) / 1e9, "unit": UNIT, "h2d_bytes_per_step": 8 * N_ROOTS,
+                "d2h_bytes_per_step": int(d2h) * N_ROOTS,
+                "api": "BfsEngine.run(source) -> BfsResult with host predecessor, per root"},
         "validation": {"roots": n_val, "passed": n_ok,
                        "method": "GPU Validator: the 5 rules of validate.py (tree edges, levels, spans, coverage)"},
-        "gpu_launches": int(len(my) * 2),  # bfs_reset_all + bfs_persistent per root
+        "gpu_launches": int(sweeps * len(my) * 2),  # bfs_reset_all + bfs_persistent per root
         "clocks": clk.summary(),
-        "timed_wall_ms": wall_ms,
+        "timed_wall_ms_per_step": wall_ms / sweeps,
     }
-    if not args.no_cpu_baseline and args.profile_roots == 0:
+    if world > 1:
+        # roots are independent: total raw pairs of the sweep / per-GPU sweep time
+        line["replica_throughput_gteps"] = float(raw[got].sum()) / (sweep_ms / 1e3) / 1e9
+    if not args.no_cpu_baseline and not args.profile_roots and world == 1:
         try:
-            import oracle
-
-            oracle.build()
-            go = oracle.Csr(g2.n, g2.row_starts, g2.dst, g2.degrees)
-            threads = os.cpu_count() or 1
-            v, used = cpu_bfs_sample({"g2": go}, roots, raw, args.cpu_seconds, threads=threads)
-            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                                    "sample": f"{used} seeded roots of the same RCM graph, oracle C port of "
-                                              f"BfsEngine hybrid, OpenMP {threads} threads"}
+            line["cpu_baseline"] = cpu_baseline_sample(g2, roots, raw, args.cpu_seconds)
         except Exception as ex:  # pragma: no cover
             line["cpu_baseline"] = {"value": None, "error": repr(ex)}
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def cpu_baseline_sample(g2, roots, raw, seconds):
+    """The oracle port of BfsEngine (hybrid_reduced, the paper's best CPU mode,
+    all host threads) on the host copy of the same RCM graph, bounded sample."""
+    import oracle
+
+    oracle.build()
+    go = oracle.Csr(g2.n, g2.row_starts, g2.dst, g2.degrees)
+    gd = oracle.degree_sort_rows(go, True)
+    threads = os.cpu_count() or 1
+    v, used = cpu_sample(go, gd, roots, raw, "hybrid_reduced", threads, seconds)
+    return {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{used} seeded roots of the same RCM graph, oracle C port of BfsEngine hybrid_reduced "
+                      f"(Alg. 6), OpenMP {threads} threads"}
 
 
 def run_partitioned(args, rb, torch, dist, g2, stats, roots, raw, world, rank, prep):
@@ -499,11 +580,11 @@ def run_partitioned(args, rb, torch, dist, g2, stats, roots, raw, world, rank, p
     local = GpuLocalLevel(g2, bounds, rank, alpha=64, beta=8, hybrid=args.mode != "level_sync")
     drv = PartitionedBfs(local, bounds, rank, world, n_policy=g2.n, m_directed=g2.m_directed,
                          hybrid=args.mode != "level_sync")
-    k = args.steps if args.profile_roots == 0 else args.profile_roots
-    order = list(range(64))
-    my = [order[i % 64] for i in range(k)]
+    my = list(range(N_ROOTS)) if not args.profile_roots else list(range(args.profile_roots))
+    sweeps = 1 if args.profile_roots else args.steps
     for i in range(args.warmup):
-        drv.run(int(roots[my[i % len(my)]]), int(deg_host[roots[my[i % len(my)]]]))
+        for j in my:
+            drv.run(int(roots[j]), int(deg_host[roots[j]]))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     ev_a = torch.cuda.Event(enable_timing=True)
     ev_b = torch.cuda.Event(enable_timing=True)
@@ -511,7 +592,7 @@ def run_partitioned(args, rb, torch, dist, g2, stats, roots, raw, world, rank, p
     dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
-        for j in my:
+        for j in [j for _ in range(sweeps) for j in my]:
             flush.zero_()
             dist.barrier()
             torch.cuda.synchronize()
@@ -547,8 +628,8 @@ def run_partitioned(args, rb, torch, dist, g2, stats, roots, raw, world, rank, p
         peak, peak_kind = measured_peak()
         ach = float(np.sum(alg) / np.sum(times) / 1e9) / world  # per GPU
         line = {
-            "metric": METRIC, "value": hmean(teps) / 1e9, "unit": UNIT, "n_gpus": world, "steps": len(my),
-            "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True,
+            "metric": METRIC, "value": hmean(teps) / 1e9, "unit": UNIT, "n_gpus": world, "steps": sweeps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * float(np.sum(times)) / sweeps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int32",
             "data": workload(args)[1] + ", built on device",
             "config": {"workload": workload(args)[0], "scale": args.scale,

@@ -1567,6 +1567,7 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
   __shared__ long long s_mf0;  // deg(src) at a traversal start (one load per CTA, not per thread)
   if (threadIdx.x == 0) {
     s_bu_next[0] = s_bu_next[1] = 0u;
+    s_p1 = 0u;
     s_ctr[4] = 0ull;  // no unvisited list yet
     if (p.mf0 < 0) s_mf0 = (long long)rb::ld_relaxed_u64((const unsigned long long*)&p.fin->mf);
   }
@@ -1657,7 +1658,6 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
     if (blockIdx.x == 0 && threadIdx.x < sizeof(Slot) / 8)
       reinterpret_cast<unsigned long long*>(p.slots + r1)[threadIdx.x] = 0ull;
     if (threadIdx.x == 0) s_bu_next[(L + 1) & 1] = 0u;  // the next level's counter (idle during this one)
-    if (threadIdx.x == 0) s_p1 = 0u;  // (read after this level's block reduction, a __syncthreads later)
 
     // Execution direction.  The level keeps the reference policy's label
     // (records, next decisions); the work is done the cheaper way.  Same next
@@ -1757,7 +1757,10 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
     if (p.dbg && (threadIdx.x & 31) == 0 && done < 64)  // RB_DEBUG_TS: per-warp end of work
       p.dbg[kDbgWarpBase + ((uint64_t)done * gridDim.x + blockIdx.x) * kWarps + (threadIdx.x >> 5)] = globaltimer();
     block_add3(s_red, acc, out);  // (its __syncthreads also orders the CTA's s_p1 updates)
-    if (kPart && p.count_p1 && threadIdx.x == 0 && s_p1) atomicAdd(&out->pad3, (unsigned long long)s_p1);
+    if (kPart && threadIdx.x == 0 && s_p1) {  // re-armed here: the next adds follow the closing grid barrier
+      atomicAdd(&out->pad3, (unsigned long long)s_p1);
+      s_p1 = 0u;
+    }
     const uint64_t tB = globaltimer();
     {
       if constexpr (kSparseOK) {
