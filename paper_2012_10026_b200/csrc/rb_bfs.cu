@@ -75,9 +75,6 @@ constexpr int kThreads = RB_THREADS;
 #ifndef RB_BU_DEFER_CONT
 #define RB_BU_DEFER_CONT 1  // bottom-up: continuation rows queued per warp and run 32 at a time
 #endif
-#ifndef RB_HOTD
-#define RB_HOTD 1  // bottom-up round 1 reads ONE 8-byte record per vertex: both scan-first neighbours + degree
-#endif
 #define RB_LEVEL_FN __device__  // (tried __noinline__ level bodies: call-ABI spills, s26 +35%)
 #ifndef RB_MINB
 #define RB_MINB 1
@@ -161,11 +158,6 @@ struct KParams {
   const int32_t* col_bu;
   const int32_t* deg;
   const int2* hot;  // per vertex: the first two neighbours in bottom-up scan order (-1 = none)
-  // packed bottom-up record (RB_HOTD): bits [0, hb) = first neighbour + 1, [hb, 2 hb) = second + 1
-  // (0 = none), [2 hb, 64) = degree saturated at dsat (then read deg[])
-  const uint64_t* hotd;
-  int32_t hb;
-  uint32_t dsat;
   int64_t n_dev;
   int64_t n_words;  // multiple of 32 * kUB
   uint32_t* vis;
@@ -294,15 +286,6 @@ __device__ __forceinline__ void ld_vinfo(const KParams& p, int64_t v, int64_t& s
   if (d == kVdSat) d = (uint32_t)(rb::ldg_i64(p.td_rs + v + 1) - s);  // degree >= 2^24: rare
   n0 = a.z;
   n1 = a.w;
-}
-
-// Packed bottom-up record -> (first, second scan-first neighbour or -1, degree;
-// the degree saturates at dsat: callers that need it exactly read deg[]).
-__device__ __forceinline__ void unpack_hot(const KParams& p, uint64_t x, int32_t& n0, int32_t& n1, uint32_t& d) {
-  const uint64_t m = (1ull << p.hb) - 1;
-  n0 = (int32_t)(x & m) - 1;
-  n1 = (int32_t)((x >> p.hb) & m) - 1;
-  d = (uint32_t)(x >> (2 * p.hb));
 }
 
 // Warp-collective claim of KU edges per lane (v[k] -> w[k], act[k]).
@@ -975,16 +958,6 @@ RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uin
     // compact side record, coalesced -- all KB loads in flight
     int2 hv[KB];
     uint32_t dg[KB];
-#if RB_HOTD
-    {
-      const uint64_t* const hotd = p.hotd + vbase;
-      uint64_t hx[KB];
-#pragma unroll
-      for (int k = 0; k < KB; ++k) hx[k] = ((actm >> k) & 1u) ? __ldg(reinterpret_cast<const unsigned long long*>(hotd + 32 * k)) : 0ull;
-#pragma unroll
-      for (int k = 0; k < KB; ++k) unpack_hot(p, hx[k], hv[k].x, hv[k].y, dg[k]);
-    }
-#else
     const int2* const hot = p.hot + vbase;
 #pragma unroll
     for (int k = 0; k < KB; ++k) {
@@ -995,7 +968,6 @@ RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uin
         dg[k] = (uint32_t)__ldg(deg + 32 * k);
       }
     }
-#endif
     uint32_t hb0[KB], hb1[KB];
 #pragma unroll
     for (int k = 0; k < KB; ++k) {
@@ -1011,9 +983,6 @@ RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uin
       const bool h0 = act && hv[k].x >= 0 && ((hb0[k] >> (hv[k].x & 31)) & 1u);
       const bool h1 = act && !h0 && hv[k].y >= 0 && ((hb1[k] >> (hv[k].y & 31)) & 1u);
       const bool found = h0 || h1;
-#if RB_HOTD
-      if (found && dg[k] == p.dsat) dg[k] = (uint32_t)__ldg(deg + 32 * k);  // saturated: the exact degree (rare)
-#endif
       h0m += h0 ? 1u : 0u;
       checks += act ? (h0 ? 1u : min(dg[k], 2u)) : 0u;  // (a second-neighbour hit implies dg >= 2)
       if (found) par_out[32 * k] = h0 ? hv[k].x : hv[k].y;
@@ -1211,14 +1180,8 @@ __device__ void bu_sparse_pass(const KParams& p, int64_t L, const uint32_t* fcur
       v = (int32_t)__ldcg(lin + t);
       if (!((ld_bits(p.vis + (v >> 5)) >> (v & 31)) & 1u)) {  // (a top-down level may have found it since)
         live = true;
-#if RB_HOTD
-        int2 h;
-        unpack_hot(p, __ldg(reinterpret_cast<const unsigned long long*>(p.hotd + v)), h.x, h.y, d);
-        if (d == p.dsat) d = (uint32_t)rb::ldg_i32(p.deg + v);
-#else
         const int2 h = __ldg(p.hot + v);
         d = (uint32_t)rb::ldg_i32(p.deg + v);
-#endif
         const uint32_t b0 = h.x >= 0 ? ld_bits(fcur + (h.x >> 5)) : 0u;
         const uint32_t b1 = h.y >= 0 ? ld_bits(fcur + (h.y >> 5)) : 0u;
         if (h.x >= 0 && ((b0 >> (h.x & 31)) & 1u)) {
@@ -1940,20 +1903,6 @@ __global__ void make_hot(const int64_t* rs, const int32_t* col, int64_t n, int r
   }
 }
 
-// packed bottom-up record (see KParams::hotd)
-__global__ void make_hotd(const int64_t* rs, const int32_t* col, int64_t n, int reverse, int hb, uint64_t* hotd) {
-  const uint64_t dsat = (hb >= 32) ? 0ull : ((1ull << (64 - 2 * hb)) - 1);
-  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t s = rs[v], e = rs[v + 1];
-    const int64_t d = e - s;
-    uint64_t a = 0, b = 0;
-    if (d > 0) a = (uint64_t)(reverse ? col[e - 1] : col[s]) + 1;
-    if (d > 1) b = (uint64_t)(reverse ? col[e - 2] : col[s + 1]) + 1;
-    const uint64_t dd = (uint64_t)d < dsat ? (uint64_t)d : dsat;
-    hotd[v] = a | (b << hb) | (dd << (2 * hb));
-  }
-}
-
 // *out += number of zero bits of words[0, n) (unvisited-at-start vertices)
 __global__ void count_zero_bits(const uint32_t* words, int64_t n, unsigned long long* out) {
   unsigned long long c = 0;
@@ -2012,7 +1961,6 @@ struct rb_bfs {
   uint32_t* vis_template;   // isolated + padding premarked
   uint32_t* pad_mask;       // padding bits only
   int2* hot;
-  uint64_t* hotd;
   VInfo* vinfo;
   VInfo* td_vinfo;  // partitioned engines only
   int64_t n_glob;
@@ -2141,7 +2089,6 @@ extern "C" int rb_bfs_create_part(const int64_t* d_row_starts, const int32_t* d_
 
   RB_ALLOC(k.parent, (size_t)n_dev * 4);
   RB_ALLOC(h->hot, (size_t)n_dev * sizeof(int2));
-  RB_ALLOC(h->hotd, (size_t)n_dev * sizeof(uint64_t));
   if (params->record_levels) RB_ALLOC(k.level, (size_t)n_dev * 4);
   RB_ALLOC(k.slots, 3 * sizeof(Slot));
   RB_ALLOC(k.bar, 64);
@@ -2161,16 +2108,6 @@ extern "C" int rb_bfs_create_part(const int64_t* d_row_starts, const int32_t* d_
   make_pad_mask<<<256, 256>>>(h->pad_mask, n_dev, h->n_words);
   make_hot<<<1024, 256>>>(d_row_starts, k.col_bu, n_dev, params->bu_reverse, h->hot);
   k.hot = h->hot;
-  {
-    // neighbour ids + 1 <= n_glob (columns are global ids in a partition)
-    const int64_t idmax = part ? part->n_glob : n_dev;
-    int hb = 1;
-    while (hb < 31 && ((int64_t)1 << hb) <= idmax) ++hb;
-    k.hb = hb;
-    k.dsat = (uint32_t)((1ull << (64 - 2 * hb)) - 1 < 0xffffffffull ? (1ull << (64 - 2 * hb)) - 1 : 0xffffffffull);
-    make_hotd<<<1024, 256>>>(d_row_starts, k.col_bu, n_dev, params->bu_reverse, hb, h->hotd);
-    k.hotd = h->hotd;
-  }
   make_vinfo<<<1024, 256>>>(d_row_starts, d_col, n_dev, h->vinfo);
   k.vinfo = h->vinfo;
   k.hubs0 = -1;
@@ -2240,7 +2177,7 @@ extern "C" int rb_bfs_destroy(rb_bfs* h) {
   if (!h) return RB_OK;
   KParams& k = h->kp;
   void* ptrs[] = {k.vis, k.fb0, k.fb1, k.fb2, h->vis_template, h->pad_mask, k.hq0, k.hq1, k.hs0, k.hs1, k.ul0, k.ul1, k.solo_q, k.parent,
-                  k.level, k.slots, k.bar, k.rec, k.fin, k.nz0, k.nz1, k.nz2, h->hot, h->hotd, h->vinfo, k.dbg, h->td_vinfo,
+                  k.level, k.slots, k.bar, k.rec, k.fin, k.nz0, k.nz1, k.nz2, h->hot, h->vinfo, k.dbg, h->td_vinfo,
                   h->part_dev};
   for (void* q : ptrs)
     if (q) cudaFree(q);

@@ -215,6 +215,70 @@ __global__ void cc_hook_heavy(const int64_t* __restrict__ rs, const int32_t* __r
   }
 }
 
+// Afforest-style components (rank space, root = min rank): every vertex first
+// hooks its first kSample neighbours (short chains, spread over all roots);
+// after compression the most frequent root is the giant component's, and the
+// full edge pass skips every vertex already in it -- an edge leaving the
+// giant set is still seen from its other endpoint, whose row is processed
+// (the CSR holds both directions).  Replaces hooking all 2m edges, which
+// hot-spots atomics on the giant component's root.
+constexpr int kSample = 2;
+
+__global__ void cc_sample(const int64_t* __restrict__ rs, const int32_t* __restrict__ col,
+                          const uint32_t* __restrict__ rank, int64_t n, int32_t* uf) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = rs[v], e = rs[v + 1];
+    if (e == s) continue;
+    const int32_t rv = (int32_t)rank[v];
+    for (int64_t j = s; j < e && j < s + kSample; ++j) {
+      const int32_t rw = (int32_t)rank[col[j]];
+      if (rw != rv) uf_hook(uf, rv, rw);
+    }
+  }
+}
+
+__global__ void cc_compress(int32_t* uf, int64_t k) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < k; r += (int64_t)gridDim.x * blockDim.x)
+    uf[r] = uf_rep(uf, (int32_t)r);
+}
+
+// the root of sample i (i < 1024): ranks spread evenly over [0, k)
+__global__ void cc_probe_roots(const int32_t* uf, int64_t k, int32_t* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < 1024) out[i] = uf_rep(const_cast<int32_t*>(uf), (int32_t)(((int64_t)i * k) / 1024));
+}
+
+__global__ void cc_hook_rest_light(const int64_t* __restrict__ rs, const int32_t* __restrict__ col,
+                                   const uint32_t* __restrict__ rank, int64_t n, int32_t giant, int32_t* uf) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = rs[v] + kSample, e = rs[v + 1];
+    if (e - s > 32 || e <= s) continue;
+    const int32_t rv = (int32_t)rank[v];
+    if (uf_rep(uf, rv) == giant) continue;
+    for (int64_t j = s; j < e; ++j) {
+      const int32_t rw = (int32_t)rank[col[j]];
+      if (rw != rv) uf_hook(uf, rv, rw);
+    }
+  }
+}
+
+__global__ void cc_hook_rest_heavy(const int64_t* __restrict__ rs, const int32_t* __restrict__ col,
+                                   const uint32_t* __restrict__ rank, int64_t n, int32_t giant, int32_t* uf) {
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int64_t v = warp; v < n; v += nwarps) {
+    const int64_t s = rs[v] + kSample, e = rs[v + 1];
+    if (e - s <= 32) continue;
+    const int32_t rv = (int32_t)rank[v];
+    if (uf_rep(uf, rv) == giant) continue;  // (warp-uniform)
+    for (int64_t j = s + lane; j < e; j += 32) {
+      const int32_t rw = (int32_t)rank[col[j]];
+      if (rw != rv) uf_hook(uf, rv, rw);
+    }
+  }
+}
+
 __global__ void cc_finalize(int32_t* uf, int64_t k, uint32_t* comp_size) {
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < k; r += (int64_t)gridDim.x * blockDim.x) {
     int32_t x = (int32_t)r;
@@ -658,8 +722,31 @@ extern "C" int rb_rcm(const int64_t* d_rs, const int32_t* d_col, const int32_t* 
   }
   // 2. components in rank space (root = min rank = the walk's seed)
   iota_u32<<<grid_for(k), 256, 0, s>>>((uint32_t*)w.uf, k);
-  cc_hook_light<<<grid_for(n), 256, 0, s>>>(d_rs, d_col, w.rank, n, w.uf);
-  cc_hook_heavy<<<grid_for(n * 32), 256, 0, s>>>(d_rs, d_col, w.rank, n, w.uf);
+  if (getenv("RB_CC_FULL")) {  // (A/B reference: hook every edge)
+    cc_hook_light<<<grid_for(n), 256, 0, s>>>(d_rs, d_col, w.rank, n, w.uf);
+    cc_hook_heavy<<<grid_for(n * 32), 256, 0, s>>>(d_rs, d_col, w.rank, n, w.uf);
+  } else {
+    cc_sample<<<grid_for(n), 256, 0, s>>>(d_rs, d_col, w.rank, n, w.uf);
+    cc_compress<<<grid_for(k), 256, 0, s>>>(w.uf, k);
+    int32_t* probe = reinterpret_cast<int32_t*>(w.keys_a);  // (scratch: the level keys are unused yet)
+    cc_probe_roots<<<4, 256, 0, s>>>(w.uf, k, probe);
+    std::vector<int32_t> h(1024);
+    RB_CUDA_TRY(cudaMemcpyAsync(h.data(), probe, 1024 * 4, cudaMemcpyDeviceToHost, s));
+    RB_CUDA_TRY(cudaStreamSynchronize(s));
+    std::sort(h.begin(), h.end());
+    int32_t giant = h[0];
+    for (size_t i = 0, best = 0; i < h.size();) {  // most frequent sampled root
+      size_t j = i;
+      while (j < h.size() && h[j] == h[i]) ++j;
+      if (j - i > best) {
+        best = j - i;
+        giant = h[i];
+      }
+      i = j;
+    }
+    cc_hook_rest_light<<<grid_for(n), 256, 0, s>>>(d_rs, d_col, w.rank, n, giant, w.uf);
+    cc_hook_rest_heavy<<<grid_for(n * 32), 256, 0, s>>>(d_rs, d_col, w.rank, n, giant, w.uf);
+  }
   cc_finalize<<<grid_for(k), 256, 0, s>>>(w.uf, k, w.comp_size);
   RB_CUDA_TRY(cudaMemsetAsync(w.comp_size, 0, (size_t)k * 4, s));
   cc_sizes<<<grid_for(k + 31), 256, 0, s>>>(w.uf, k, w.comp_size);

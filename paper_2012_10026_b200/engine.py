@@ -295,27 +295,36 @@ class _DeviceBfs:
     def run_to_host(self, source: int, n: int, chunks: int = 0):
         """BfsEngine.run's result path: reset + launch, then -- all enqueued
         behind the traversal -- the launch state, the level records and the
-        parents [0, n_dev) in chunks into the pinned staging buffer.  While
-        the GPU works the host allocates the result array (fresh, hugepage
-        backed) and fills the isolated tail with -1; each landed chunk is
-        copied out by torch's multi-threaded copy.  One wait for the small
-        copies, one per chunk.  Returns (predecessor, records, seconds)."""
+        parents [0, n_dev).  Large results go straight into the fresh result
+        array (a pooled hugepage mapping page-locked once, so one DMA and no
+        host copy); small ones through the pinned staging buffer in chunks,
+        each landed chunk copied out while the next is in flight.  The
+        isolated tail is filled with -1 while the GPU works.  Returns
+        (predecessor, records, seconds)."""
         torch = self.torch
         L = _lib.lib()
         s = _lib.stream_ptr()
         self.traverse(source)
         if self._state is None:
             self._state = torch.empty(int(L.rb_bfs_state_bytes()) // 8, dtype=torch.int64, pin_memory=True)
-            self._recs_pin = torch.empty(_REC_FAST * 10, dtype=torch.int64, pin_memory=True)
+            self._recs_pin = torch.empty(_REC_FAST * ctypes.sizeof(_lib.LevelRecordC) // 8, dtype=torch.int64,
+                                         pin_memory=True)
         n_dev = self.n_dev
-        # 8 pieces by default (the ABI accepts 1..32): measured best at s22 and s26
-        # (1 / 2 / 4 / 8 -> 128 / 146 / 156 / 159 e2e GTEPS at s22; 16 / 32 lose)
-        chunks = chunks or int(os.environ.get("RB_E2E_CHUNKS", "0")) or 8
-        if not 1 <= chunks <= _MAX_CHUNKS:
-            raise ValueError(f"result chunks must be in [1, {_MAX_CHUNKS}], got {chunks}")
+        pred, registered = fresh_int32(n, want_registered=True)
+        if registered:
+            # the result array is page-locked (pooled, registered once): the
+            # parents are DMA'd straight into it in one copy, no staging hop
+            chunks = 1
+            dst = pred.ctypes.data
+        else:
+            # 8 pieces by default (the ABI accepts 1..32): measured best at s22 and s26
+            # (1 / 2 / 4 / 8 -> 128 / 146 / 156 / 159 e2e GTEPS at s22; 16 / 32 lose)
+            chunks = chunks or int(os.environ.get("RB_E2E_CHUNKS", "0")) or 8
+            if not 1 <= chunks <= _MAX_CHUNKS:
+                raise ValueError(f"result chunks must be in [1, {_MAX_CHUNKS}], got {chunks}")
+            dst = _lib.ptr(self.pinned)
         _lib.check(L.rb_bfs_results_async(self.h, _lib.ptr(self._state), _lib.ptr(self._recs_pin), _REC_FAST,
-                                          _lib.ptr(self.pinned), chunks, s), "rb_bfs_results_async")
-        pred = fresh_int32(n)
+                                          dst, chunks, s), "rb_bfs_results_async")
         pt = torch.from_numpy(pred)
         if n > n_dev:
             pt[n_dev:].fill_(-1)
@@ -330,7 +339,7 @@ class _DeviceBfs:
             for i in range(chunks):
                 a, b = i * step, min((i + 1) * step, n_dev)
                 _lib.check(L.rb_bfs_wait(self.h, i), "rb_bfs_wait")
-                if b > a:
+                if b > a and not registered:
                     pt[a:b].copy_(self.pinned[a:b])
             el = ctypes.c_double(0.0)
             _lib.check(L.rb_bfs_elapsed(self.h, ctypes.byref(el)), "rb_bfs_elapsed")
@@ -399,8 +408,9 @@ class _ResultPool:
         self.keep = keep
         self.free: dict[int, list] = {}
         self.lock = threading.Lock()
+        self.registered: set[int] = set()  # id() of mappings page-locked with cudaHostRegister
 
-    def get(self, nbytes: int):
+    def get(self, nbytes: int, register: bool = False):
         with self.lock:
             lst = self.free.get(nbytes)
             if lst:
@@ -408,6 +418,14 @@ class _ResultPool:
         m = mmap.mmap(-1, nbytes, flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
         if hasattr(m, "madvise") and hasattr(mmap, "MADV_HUGEPAGE"):
             m.madvise(mmap.MADV_HUGEPAGE)
+        if register:
+            # page-locked once for the life of the mapping (pool entries are never
+            # unmapped), so the device copies straight into the result array
+            import torch
+
+            addr = ctypes.addressof(ctypes.c_char.from_buffer(m))
+            if int(torch.cuda.cudart().cudaHostRegister(addr, nbytes, 0)) == 0:
+                self.registered.add(id(m))
         return m
 
     def put(self, m):
@@ -415,22 +433,34 @@ class _ResultPool:
             lst = self.free.setdefault(len(m), [])
             if len(lst) < self.keep:
                 lst.append(m)
+                return
+            registered = id(m) in self.registered
+            self.registered.discard(id(m))
+        if registered:  # dropped from the pool: unlock before the mapping goes away
+            import torch
+
+            torch.cuda.cudart().cudaHostUnregister(ctypes.addressof(ctypes.c_char.from_buffer(m)))
 
 
 _POOL = _ResultPool()
 
 
-def fresh_int32(n: int) -> np.ndarray:
+def fresh_int32(n: int, want_registered: bool = False):
     """A new int32 array of n entries (contents undefined).  Up to 32 MB:
     np.empty (glibc reuses already-faulted heap pages).  Larger: a pooled
     hugepage mapping (see _ResultPool) -- first touch of fresh 4 KB pages
-    runs at ~8 GB/s, a warm pooled buffer is written at ~50 GB/s."""
+    runs at ~8 GB/s, a warm pooled buffer is written at ~50 GB/s; with
+    ``want_registered`` the mapping is also page-locked (RB_E2E_REGISTER=0
+    turns that off) and (array, registered) is returned."""
     if n < (8 << 20):
-        return np.empty(n, dtype=np.int32)
-    m = _POOL.get(4 * n)
+        a = np.empty(n, dtype=np.int32)
+        return (a, False) if want_registered else a
+    reg = want_registered and os.environ.get("RB_E2E_REGISTER", "1") != "0"
+    m = _POOL.get(4 * n, register=reg)
     h = _Holder(m)
     weakref.finalize(h, _POOL.put, m)
-    return np.frombuffer(h, dtype=np.int32)
+    a = np.frombuffer(h, dtype=np.int32)
+    return (a, id(m) in _POOL.registered) if want_registered else a
 
 
 def _records_to_levels(recs, part=None) -> list:

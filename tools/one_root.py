@@ -12,10 +12,15 @@ import paper_2012_10026_b200 as rb  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--scale", type=int, default=26)
 ap.add_argument("--index", type=int, default=0)
+ap.add_argument("--graph", default="kronecker", choices=["kronecker", "chunglu"])
+ap.add_argument("--no-warmup", action="store_true", help="profile the first run (ncu flushes caches per replay)")
 a = ap.parse_args()
 import torch  # noqa: E402
 
-el = rb.kronecker_generate(rb.KroneckerParams(scale=a.scale), device=True)
+if a.graph == "chunglu":
+    el = rb.chunglu_generate(rb.ChungLuParams(n=1 << a.scale), device=True)
+else:
+    el = rb.kronecker_generate(rb.KroneckerParams(scale=a.scale), device=True)
 g = rb.build_csr(el)
 del el
 perm, st = rb.rcm(g)
@@ -25,7 +30,8 @@ roots = rb.sample_sources(g2.device_arrays()[2].cpu().numpy(), 64, 1)
 s = int(roots[a.index])
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 with rb.BfsEngine(g2, rb.BfsParams()) as eng:
-    eng.run_device(s)
+    if not a.no_warmup:
+        eng.run_device(s)
     flush.zero_()
     t, levels = eng.run_device(s)
     print(f"root {s} (index {a.index}): {t * 1e6:.1f} us")
