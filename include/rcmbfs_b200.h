@@ -145,6 +145,31 @@ int rb_bfs_reset_part(rb_bfs* h, int64_t source_global, void* stream);
 int rb_bfs_dist_level(rb_bfs* h, int64_t level, int direction, int hubs, const uint32_t* d_fcur_glob,
                       const uint8_t* d_nz_glob, uint32_t** d_next_local, int64_t* h_counters, void* stream);
 int rb_bfs_words(rb_bfs* h, int64_t* n_words_local, int64_t* n_words_glob);
+
+/* Device-side exchange for the 1D partition (the level loop stays on the
+ * device; replaces the per-level all-gather / all-reduce of the host-driven
+ * path above).  Per rank: rb_bfs_xchg_alloc (three global frontier bitmaps +
+ * summaries, counter slots, barrier counter in one allocation), then either
+ *   multi-process: rb_bfs_xchg_handle -> exchange the world handles (e.g.
+ *   torch.distributed.all_gather_object) -> rb_bfs_xchg_open (cudaIpc, NVLink
+ *   peer mappings), and per root rb_bfs_dist_reset + rb_bfs_dist_traverse on
+ *   every rank (ONE persistent launch each: at every level a rank stores its
+ *   next-frontier words and counters into every peer's buffers and meets the
+ *   others at a system-scope barrier), rb_bfs_dist_results;
+ *   one GPU (emulation of `world` ranks): rb_bfs_xchg_connect_local over the
+ *   ranks' engines of this process, rb_bfs_dist_reset each, then
+ *   rb_bfs_dist_traverse_emu (ONE cooperative launch over all ranks' data).
+ * Records are written by rank 0's engine.  world <= 8; v_lo % 128 == 0. */
+int rb_bfs_xchg_alloc(rb_bfs* h, int32_t world, int32_t rank);
+size_t rb_bfs_xchg_handle_bytes(void);
+int rb_bfs_xchg_handle(rb_bfs* h, void* h_handle_out);
+int rb_bfs_xchg_open(rb_bfs* h, const void* h_handles /* world handles, rank order */);
+int rb_bfs_xchg_connect_local(rb_bfs* const* hs, int32_t world);
+int rb_bfs_dist_reset(rb_bfs* h, int64_t source_global, int64_t deg_source, void* stream);
+int rb_bfs_dist_traverse(rb_bfs* h, void* stream);
+int rb_bfs_dist_traverse_emu(rb_bfs* const* hs, int32_t world, void* stream);
+int rb_bfs_dist_results(rb_bfs* h, rb_level_record* h_records, int64_t cap, int64_t* n_records, double* elapsed_s,
+                        void* stream);
 /* Nonzero summary of a bitmap: d_nz[i] = (d_words[i] != 0), one byte per word. */
 int rb_make_nz(const uint32_t* d_words, int64_t n_words, uint8_t* d_nz, void* stream);
 /* Transpose slice for a partition: for every global vertex u < n_glob, the

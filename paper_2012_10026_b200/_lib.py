@@ -68,6 +68,22 @@ _SIGS = {
     "rb_transpose_rows": ([P, P, I64, I64, I64, I64, P, SZ, P, P, P], ctypes.c_int),
     "rb_bfs_reset": ([P, I64, P], ctypes.c_int),
     "rb_bfs_set_partitions": ([P, P, I64, I64, I32], ctypes.c_int),
+    "rb_bfs_xchg_alloc": ([P, I32, I32], ctypes.c_int),
+    "rb_kronecker_generate_range": ([ctypes.c_int, I64, ctypes.c_uint64, ctypes.c_double, ctypes.c_double,
+                                     ctypes.c_double, I64, I64, P, P], ctypes.c_int),
+    "rb_csr_keys": ([P, ctypes.POINTER(P), ctypes.POINTER(I64)], ctypes.c_int),
+    "rb_keys_workspace_bytes": ([I64], SZ),
+    "rb_keys_sort_unique": ([P, I64, ctypes.c_int, P, SZ, ctypes.POINTER(I64), P], ctypes.c_int),
+    "rb_keys_to_csr": ([P, I64, I64, I64, P, P, P, P], ctypes.c_int),
+    "rb_relabel_keys": ([P, P, I64, I64, P, P, P], ctypes.c_int),
+    "rb_bfs_xchg_handle_bytes": ([], SZ),
+    "rb_bfs_xchg_handle": ([P, P], ctypes.c_int),
+    "rb_bfs_xchg_open": ([P, P], ctypes.c_int),
+    "rb_bfs_xchg_connect_local": ([P, I32], ctypes.c_int),
+    "rb_bfs_dist_reset": ([P, I64, I64, P], ctypes.c_int),
+    "rb_bfs_dist_traverse": ([P, P], ctypes.c_int),
+    "rb_bfs_dist_traverse_emu": ([P, I32, P], ctypes.c_int),
+    "rb_bfs_dist_results": ([P, P, I64, ctypes.POINTER(I64), ctypes.POINTER(ctypes.c_double), P], ctypes.c_int),
     "rb_bfs_traverse": ([P, P], ctypes.c_int),
     "rb_bfs_elapsed": ([P, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
     "rb_bfs_results": ([P, P, P, P, I64, ctypes.POINTER(I64), P], ctypes.c_int),

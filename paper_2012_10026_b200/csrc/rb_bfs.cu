@@ -58,6 +58,8 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+
+#include <algorithm>
 #include <vector>
 
 #include "rb_common.cuh"
@@ -1946,6 +1948,341 @@ __global__ void make_pad_mask(uint32_t* m, int64_t n_dev, int64_t n_words) {
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// 1D-partitioned traversal with the exchange on the device.
+//
+// Rank r owns global vertices [v_lo, v_lo + n_dev): its CSR rows (global
+// column ids; bottom-up), the transpose slice (the owned neighbours of every
+// global vertex; top-down), its visited words and parents -- exactly the
+// rb_bfs_create_part engine.  Instead of the host driving one launch per
+// level, ONE persistent launch per rank runs the whole level loop:
+//   1. the level's local work (top-down claims through the transpose slice or
+//      bottom-up finds over the owned rows, both against the GLOBAL frontier
+//      bitmap xg[L % 3]) into the local next-frontier words;
+//   2. publish: the nonzero local next-frontier words (and their summary
+//      bytes) are stored straight into EVERY rank's xg[(L + 1) % 3] at this
+//      rank's word offset -- peer memory over NVLink (CUDA IPC mappings) --
+//      and the level totals {n_next, deg_next, maxdeg, scanned} into every
+//      rank's counter slot [L & 1][r];
+//   3. one cross-GPU barrier (system-scope release adds on every peer's
+//      counter, acquire spin on the own one), then every rank sums the slots:
+//      the same global counters drive update_traversal_policy on all ranks.
+// xg is triple-buffered: during level L a rank zeroes its xg[(L + 2) % 3],
+// which nobody reads any more (level L - 1's frontier) and nobody writes
+// before the barrier that ends level L.  No host round trip per level.
+//
+// Emulation (one GPU, the profiling guide's rule for fewer GPUs than ranks):
+// bfs_dist_emu runs all ranks' data in ONE cooperative launch, the ranks'
+// level work one after the other with the whole grid, the publish identical,
+// and the cross-rank barrier a grid barrier.
+
+constexpr int kMaxWorld = 8;
+
+struct XParams {
+  int32_t world, rank;
+  int64_t n_words_glob;
+  int64_t w_lo;                                // this rank's first global word (v_lo / 32)
+  uint32_t* xg[3];                             // own global frontier bitmaps
+  uint8_t* xnz[3];                             // their summaries (one byte per word)
+  unsigned long long* slot;                    // own counter slots [2][kMaxWorld][4]
+  uint32_t* xbar;                              // own cross-rank barrier counter (never reset)
+  uint32_t* peer_xg[kMaxWorld][3];             // every rank's xg / xnz / slot / xbar as seen from here
+  uint8_t* peer_xnz[kMaxWorld][3];
+  unsigned long long* peer_slot[kMaxWorld];
+  uint32_t* peer_xbar[kMaxWorld];
+  uint32_t xepoch0;                            // cross barriers completed before this launch
+};
+
+__device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void red_release_sys_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+struct DistShared {
+  unsigned long long red[kWarps * 4];
+  unsigned long long ctr[5];
+  uint32_t bu_found[kWarps][kBU];
+  uint32_t bu_pair[kWarps][32 * kBU + 64 > kList ? 32 * kBU + 64 : kList];
+  uint32_t next_step;
+};
+
+// One rank's work of level L (local claims / finds), ending with a grid
+// barrier that leaves this rank's level totals in sm.ctr[0..3] (n_next,
+// deg_next, maxdeg, scanned).  nblocks = the grid; epoch = its barrier count.
+template <bool kRev, int KB>
+__device__ void dist_body(const KParams& p, const XParams& x, int64_t L, int xdir, bool hubs, int64_t nf,
+                          int64_t mf, int64_t mu, uint32_t& epoch, DistShared& sm) {
+  const int r0 = (int)(L % 3), r1 = (r0 + 1) % 3, r2 = (r0 + 2) % 3;
+  const uint32_t nblocks = gridDim.x;
+  const uint64_t gtid = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
+  const uint64_t gthreads = (uint64_t)nblocks * kThreads;
+  Slot* out = p.slots + r0;
+  Slot* in = p.slots + r2;
+  const uint32_t* fcur = x.xg[r0];
+  uint32_t* fnext = fb_of(p, r1);
+  // zero ahead: the local fnext of level L+1, the global frontier of level L+2, the next counter slot
+  for (uint64_t i = gtid; i < (uint64_t)p.n_words / 4; i += gthreads) {
+    reinterpret_cast<uint4*>(fb_of(p, r2))[i] = make_uint4(0u, 0u, 0u, 0u);
+  }
+  for (uint64_t i = gtid; i < (uint64_t)p.n_words / 16; i += gthreads)
+    reinterpret_cast<uint4*>(nz_of(p, r2))[i] = make_uint4(0u, 0u, 0u, 0u);
+  for (uint64_t i = gtid; i < (uint64_t)x.n_words_glob / 4; i += gthreads)
+    reinterpret_cast<uint4*>(x.xg[r2])[i] = make_uint4(0u, 0u, 0u, 0u);
+  for (uint64_t i = gtid; i < (uint64_t)x.n_words_glob / 16; i += gthreads)
+    reinterpret_cast<uint4*>(x.xnz[r2])[i] = make_uint4(0u, 0u, 0u, 0u);
+  if (blockIdx.x == 0 && threadIdx.x < sizeof(Slot) / 8)
+    reinterpret_cast<unsigned long long*>(p.slots + r1)[threadIdx.x] = 0ull;
+  if (threadIdx.x == 0) sm.next_step = 0u;
+  __syncthreads();
+  Acc acc{0, 0, 0, 0u};
+  if (xdir == 0) {
+    QEnt* hq = (L & 1) ? p.hq1 : p.hq0;
+    uint32_t* hs = (L & 1) ? p.hs1 : p.hs0;
+    TdCtx c;
+    c.p = &p;
+    c.L = L;
+    c.fcur = fcur;
+    c.fnext = fnext;
+    c.nznext = nz_of(p, r1);
+    c.probe = 2 * mu < p.m_directed || mf >= p.probe_mf;
+    c.defer = mf >= p.defer_mf;
+    c.hub_min = (hubs && nf <= kLightToB) ? kTinyDeg : kLightDeg;
+    if (c.defer) {
+      for (uint64_t i = gtid; i < (uint64_t)p.n_words / 4; i += gthreads)
+        reinterpret_cast<uint4*>(fnext)[i] = __ldcg(reinterpret_cast<const uint4*>(p.vis) + i);
+      rb::grid_barrier(p.bar, nblocks, epoch);
+    }
+    if (nf >= kDenseFrontier)
+      td_rows_words(c, hq, hs, &in->hq_count, acc, sm.bu_pair[threadIdx.x >> 5], &sm.next_step);
+    else
+      td_rows_items(c, x.xnz[r0], hq, hs, &in->hq_count, acc, sm.bu_pair[threadIdx.x >> 5]);
+    if (hubs) {
+      const unsigned long long* const src[1] = {&in->hq_count};
+      rb::grid_barrier_fetch<1>(p.bar, nblocks, epoch, src, sm.ctr);
+      td_hubs(c, hq, hs, sm.ctr[0] >> 40, sm.ctr[0] & kSliceMask, acc);
+    }
+    if (c.defer) {
+      rb::grid_barrier(p.bar, nblocks, epoch);
+      count_next(p, fnext, nz_of(p, r1), acc);
+    }
+  } else {
+    const uint32_t wib = threadIdx.x >> 5;
+    bu_level<kRev, KB, false>(p, L, fcur, fnext, nz_of(p, r1), acc, sm.bu_found[wib], sm.bu_pair[wib],
+                              &sm.next_step, nullptr, nullptr, nullptr);
+  }
+  block_add3(sm.red, acc, out);
+  const unsigned long long* const src[4] = {&out->n_next, &out->deg_next, &out->maxdeg, &out->scanned};
+  rb::grid_barrier_fetch<4>(p.bar, nblocks, epoch, src, sm.ctr);
+}
+
+// Publish this rank's level-L results to every rank (peer stores; see above).
+__device__ void dist_publish(const KParams& p, const XParams& x, int64_t L, const unsigned long long* tot) {
+  const int r1 = (int)((L + 1) % 3);
+  const uint32_t* fnext = fb_of(p, r1);
+  const uint64_t gtid = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
+  const uint64_t gthreads = (uint64_t)gridDim.x * kThreads;
+  for (uint64_t i = gtid; i < (uint64_t)p.n_words / 4; i += gthreads) {
+    const uint4 v = __ldcg(reinterpret_cast<const uint4*>(fnext) + i);
+    if (!(v.x | v.y | v.z | v.w)) continue;  // the targets are zeroed ahead
+    const uint32_t nzb = (v.x ? 1u : 0u) | (v.y ? 0x100u : 0u) | (v.z ? 0x10000u : 0u) | (v.w ? 0x1000000u : 0u);
+    const uint64_t gw = (uint64_t)x.w_lo + 4 * i;  // w_lo % 4 == 0: 16-byte chunks never straddle two ranks
+    for (int q = 0; q < x.world; ++q) {
+      reinterpret_cast<uint4*>(x.peer_xg[q][r1] + gw)[0] = v;
+      reinterpret_cast<uint32_t*>(x.peer_xnz[q][r1] + gw)[0] = nzb;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < 4 * (uint32_t)x.world) {
+    const int q = threadIdx.x >> 2, k = threadIdx.x & 3;
+    x.peer_slot[q][((L & 1) * kMaxWorld + x.rank) * 4 + k] = tot[k];
+  }
+}
+
+// Global level totals: sum (max for maxdeg) of every rank's slot [L & 1].
+__device__ __forceinline__ void dist_totals(const XParams& x, int64_t L, unsigned long long* out4) {
+  unsigned long long a = 0, b = 0, m = 0, c = 0;
+  for (int q = 0; q < x.world; ++q) {
+    const unsigned long long* sl = x.slot + ((L & 1) * kMaxWorld + q) * 4;
+    a += rb::ld_relaxed_u64(sl + 0);
+    b += rb::ld_relaxed_u64(sl + 1);
+    m = max(m, (unsigned long long)rb::ld_relaxed_u64(sl + 2));
+    c += rb::ld_relaxed_u64(sl + 3);
+  }
+  out4[0] = a;
+  out4[1] = b;
+  out4[2] = m;
+  out4[3] = c;
+}
+
+// Grid barrier whose release waits for every rank (real multi-GPU): CTA 0
+// arrives last, after the cross-rank barrier.  All CTAs fenced their peer
+// stores at system scope before arriving.
+__device__ void grid_barrier_cross(const XParams& x, uint32_t* bar, uint32_t nblocks, uint32_t& epoch,
+                                   uint32_t& xepoch) {
+  ++epoch;
+  ++xepoch;
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t target = epoch * nblocks;
+    if (blockIdx.x == 0) {
+      while ((int32_t)(rb::ld_relaxed_u32(bar) - (target - 1)) < 0) {
+      }
+      __threadfence_system();
+      for (int q = 0; q < x.world; ++q) red_release_sys_add(x.peer_xbar[q], 1u);
+      const uint32_t xt = xepoch * (uint32_t)x.world;
+      while ((int32_t)(ld_acquire_sys_u32(x.xbar) - xt) < 0) {
+      }
+      rb::red_release_add(bar, 1u);
+    } else {
+      rb::red_release_add(bar, 1u);
+      while ((int32_t)(rb::ld_relaxed_u32(bar) - target) < 0) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Level record + policy (engine.py:587-596), identical on every rank.
+struct DistState {
+  int64_t L, nf, mf, mu, done;
+  int dir;
+  bool hubs;
+  uint64_t t_prev;
+};
+
+__device__ __forceinline__ void dist_advance(const KParams& p, bool write_rec, int xdir, const unsigned long long* g,
+                                             DistState& st) {
+  const int64_t n_next = (int64_t)g[0], deg_next = (int64_t)g[1];
+  if (write_rec && blockIdx.x == 0 && threadIdx.x == 32) {
+    const uint64_t t_now = globaltimer();
+    rb_level_record r;
+    r.level = st.L;
+    r.direction = st.dir;
+    r.n_f = st.nf;
+    r.m_f = st.mf;
+    r.m_u = st.mu;
+    r.scanned_edges = (int64_t)g[3];
+    r.t_ns = (int64_t)(t_now - st.t_prev);
+    r.n_next = n_next;
+    r.t_queue_ns = 0;
+    r.reserved = xdir;
+    r.pass1_hits = -1;
+    r.live_vertices = -1;
+    r.claimed = -1;
+    r.reserved2 = 0;
+    p.rec[st.done] = r;
+    st.t_prev = t_now;
+  }
+  st.mu -= deg_next;
+  st.mf = deg_next;
+  st.nf = n_next;
+  st.hubs = g[2] > kLightDeg;
+  int ndir = 0;
+  if (p.hybrid) {
+    if (st.dir == 0)
+      ndir = (st.mf * (int64_t)p.alpha > st.mu) ? 1 : 0;
+    else
+      ndir = (st.nf * (int64_t)p.beta < p.n_policy) ? 0 : 1;
+  }
+  st.dir = ndir;
+  ++st.L;
+  ++st.done;
+}
+
+__device__ __forceinline__ int dist_exec_dir(const KParams& p, const DistState& st) {
+  // early levels labelled bottom-up with few frontier edges run top-down (the
+  // single-GPU crossover, every input global so all ranks agree)
+  if (p.exec_opt && st.dir == 1 && 2 * st.mu > p.m_directed && st.mf * p.exec_alpha <= st.mu) return 0;
+  return st.dir;
+}
+
+__device__ __forceinline__ void dist_finish(const KParams& p, const DistState& st, uint32_t xepoch) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    p.fin->levels_done = st.done;
+    p.fin->L = st.L;
+    p.fin->dir = st.dir;
+    p.fin->nf = st.nf;
+    p.fin->mf = st.mf;
+    p.fin->mu = st.mu;
+    p.fin->pad = xepoch;  // cross barriers completed (the next launch's xepoch0)
+  }
+}
+
+// Real multi-GPU: one launch per rank, the whole level loop on the device.
+template <bool kRev, int KB>
+__global__ void __launch_bounds__(kThreads, 1) bfs_dist(KParams p, XParams x) {
+  __shared__ DistShared sm;
+  __shared__ unsigned long long s_tot[4];
+  uint32_t epoch = 0, xepoch = x.xepoch0;
+  DistState st{0, 1, p.mf0, p.mu0, 0, 0, p.mf0 > (int64_t)kLightDeg, 0};
+  if (blockIdx.x == 0 && threadIdx.x == 32) st.t_prev = globaltimer();
+  // every rank's reset (its xg[1] zeroed, its seed) is done before anyone publishes
+  grid_barrier_cross(x, p.bar, gridDim.x, epoch, xepoch);
+  while (st.done < p.max_levels && st.nf > 0) {
+    const int xdir = dist_exec_dir(p, st);
+    dist_body<kRev, KB>(p, x, st.L, xdir, st.hubs, st.nf, st.mf, st.mu, epoch, sm);
+    dist_publish(p, x, st.L, sm.ctr);
+    grid_barrier_cross(x, p.bar, gridDim.x, epoch, xepoch);
+    if (threadIdx.x == 0) dist_totals(x, st.L, s_tot);
+    __syncthreads();
+    dist_advance(p, x.rank == 0, xdir, s_tot, st);
+  }
+  dist_finish(p, st, xepoch);
+}
+
+// One GPU: the ranks' data in one cooperative launch (ranks run in turn).
+struct EmuParams {
+  int32_t world;
+  const KParams* kp;  // device arrays of world entries
+  const XParams* xp;
+};
+
+template <bool kRev, int KB>
+__global__ void __launch_bounds__(kThreads, 1) bfs_dist_emu(EmuParams e) {
+  __shared__ DistShared sm;
+  __shared__ unsigned long long s_tot[4];
+  uint32_t epoch = 0;
+  const KParams& p0 = e.kp[0];
+  DistState st{0, 1, p0.mf0, p0.mu0, 0, 0, p0.mf0 > (int64_t)kLightDeg, 0};
+  if (blockIdx.x == 0 && threadIdx.x == 32) st.t_prev = globaltimer();
+  while (st.done < p0.max_levels && st.nf > 0) {
+    const int xdir = dist_exec_dir(p0, st);
+    for (int g = 0; g < e.world; ++g) {
+      dist_body<kRev, KB>(e.kp[g], e.xp[g], st.L, xdir, st.hubs, st.nf, st.mf, st.mu, epoch, sm);
+      dist_publish(e.kp[g], e.xp[g], st.L, sm.ctr);
+    }
+    rb::grid_barrier(p0.bar, gridDim.x, epoch);  // the cross-rank barrier of the emulation
+    if (threadIdx.x == 0) dist_totals(e.xp[0], st.L, s_tot);
+    __syncthreads();
+    dist_advance(p0, true, xdir, s_tot, st);
+  }
+  for (int g = 0; g < e.world; ++g) dist_finish(e.kp[g], st, 0);
+}
+
+// Per-root reset of the exchange buffers: xg[0] = the source bit, summary;
+// xg[1], xg[2], summaries and the slots zero.
+__global__ void dist_reset_x(XParams x, int64_t src_glob) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t sw = src_glob >> 5;
+  for (int64_t i = t0; i < x.n_words_glob; i += stride) {
+    x.xg[0][i] = i == sw ? (1u << (src_glob & 31)) : 0u;
+    x.xg[1][i] = 0u;
+    x.xg[2][i] = 0u;
+    x.xnz[0][i] = i == sw ? 1u : 0u;
+    x.xnz[1][i] = 0u;
+    x.xnz[2][i] = 0u;
+  }
+  if (t0 < 2 * kMaxWorld * 4) x.slot[t0] = 0ull;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -1980,6 +2317,12 @@ struct rb_bfs {
   void* stream;
   bool exact;            // RB_PART_EXACT: run the labelled direction every level
   int32_t* part_dev;     // [n_parts + 1 block bounds | first | last]
+  // device-side exchange (rb_bfs_xchg_*): partitioned engines only
+  XParams x;
+  void* xblock;                    // xg[3] | xnz[3] | slots | xbar, one allocation (IPC-exported)
+  size_t xbytes;
+  std::vector<void*> x_opened;     // peers' blocks mapped with cudaIpcOpenMemHandle
+  int64_t src_deg;                 // deg(source) of the current distributed traversal
 };
 
 // The traversal kernel of an engine: scan direction x bottom-up step width.
@@ -2064,8 +2407,19 @@ extern "C" int rb_bfs_create_part(const int64_t* d_row_starts, const int32_t* d_
   k.n_dev = n_dev;
   k.n_words = h->n_words;
   const size_t wb = (size_t)h->n_words * 4;
-  // hub-slice queue capacity: sum over vertices of ceil(deg / kChunk)
-  const size_t nhub = (size_t)n_dev + (size_t)(params->m_directed / kChunk) + 64;
+  // hub-row queue capacity (one entry per frontier row longer than kLightDeg):
+  // single GPU n_dev rows (+ slack); a partition expands GLOBAL rows of the
+  // transpose slice, of which fewer than td_m / kLightDeg are that long
+  size_t nhub = (size_t)n_dev + (size_t)(params->m_directed / kChunk) + 64;
+  if (part) {
+    int64_t td_m = 0;
+    if (cudaMemcpy(&td_m, part->d_td_row_starts + part->n_glob, 8, cudaMemcpyDeviceToHost) != cudaSuccess) {
+      rb_set_error("rb_bfs_create: reading the transpose slice size failed");
+      rb_bfs_destroy(h);
+      return RB_ERR_CUDA;
+    }
+    nhub = std::max((size_t)n_dev, (size_t)(td_m / kLightDeg)) + (size_t)(td_m / kChunk) + 64;
+  }
   int rc = RB_OK;
 #define RB_ALLOC(ptr, bytes) \
   if (rc == RB_OK) rc = alloc_dev((void**)&(ptr), (bytes));
@@ -2181,6 +2535,8 @@ extern "C" int rb_bfs_destroy(rb_bfs* h) {
                   h->part_dev};
   for (void* q : ptrs)
     if (q) cudaFree(q);
+  for (void* b : h->x_opened) cudaIpcCloseMemHandle(b);
+  if (h->xblock) cudaFree(h->xblock);
   if (h->ev_start) cudaEventDestroy(h->ev_start);
   for (int i = 0; i <= kMaxChunks; ++i)
     if (h->ev_chunk[i]) cudaEventDestroy(h->ev_chunk[i]);
@@ -2559,6 +2915,245 @@ extern "C" int rb_bfs_dist_level(rb_bfs* h, int64_t level, int direction, int hu
   if (d_next_local) {
     const int64_t r = (level + 1) % 3;
     *d_next_local = r == 0 ? h->kp.fb0 : (r == 1 ? h->kp.fb1 : h->kp.fb2);
+  }
+  return RB_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// Device-side exchange for the 1D partition (see bfs_dist)
+
+static size_t xblock_layout(int64_t nwg, size_t off[5]) {
+  size_t o = 0;
+  auto take = [&](size_t b) { size_t r = o; o += (b + 255) & ~(size_t)255; return r; };
+  off[0] = take((size_t)3 * nwg * 4);                 // xg[3]
+  off[1] = take((size_t)3 * nwg);                     // xnz[3]
+  off[2] = take((size_t)2 * kMaxWorld * 4 * 8);       // slots
+  off[3] = take(64);                                  // xbar
+  off[4] = o;
+  return o;
+}
+
+static void xparams_self(rb_bfs* h) {
+  XParams& x = h->x;
+  size_t off[5];
+  xblock_layout(x.n_words_glob, off);
+  char* b = (char*)h->xblock;
+  for (int r = 0; r < 3; ++r) {
+    x.xg[r] = (uint32_t*)(b + off[0]) + (size_t)r * x.n_words_glob;
+    x.xnz[r] = (uint8_t*)(b + off[1]) + (size_t)r * x.n_words_glob;
+  }
+  x.slot = (unsigned long long*)(b + off[2]);
+  x.xbar = (uint32_t*)(b + off[3]);
+}
+
+static void xparams_peer(rb_bfs* h, int q, char* b) {
+  XParams& x = h->x;
+  size_t off[5];
+  xblock_layout(x.n_words_glob, off);
+  for (int r = 0; r < 3; ++r) {
+    x.peer_xg[q][r] = (uint32_t*)(b + off[0]) + (size_t)r * x.n_words_glob;
+    x.peer_xnz[q][r] = (uint8_t*)(b + off[1]) + (size_t)r * x.n_words_glob;
+  }
+  x.peer_slot[q] = (unsigned long long*)(b + off[2]);
+  x.peer_xbar[q] = (uint32_t*)(b + off[3]);
+}
+
+extern "C" int rb_bfs_xchg_alloc(rb_bfs* h, int32_t world, int32_t rank) {
+  if (!h || !h->td_vinfo || world < 1 || world > kMaxWorld || rank < 0 || rank >= world || (h->kp.v_lo % 128)) {
+    rb_set_error("rb_bfs_xchg_alloc: needs a partitioned engine with v_lo %% 128 == 0, 1 <= world <= %d, "
+                 "0 <= rank < world", kMaxWorld);
+    return RB_ERR_ARG;
+  }
+  if (h->xblock) return RB_OK;
+  XParams& x = h->x;
+  memset(&x, 0, sizeof(x));
+  x.world = world;
+  x.rank = rank;
+  x.n_words_glob = h->kp.n_words_glob;
+  x.w_lo = h->kp.v_lo / 32;
+  size_t off[5];
+  h->xbytes = xblock_layout(x.n_words_glob, off);
+  int rc = alloc_dev(&h->xblock, h->xbytes);
+  if (rc) return rc;
+  RB_CUDA_TRY(cudaMemset(h->xblock, 0, h->xbytes));
+  xparams_self(h);
+  xparams_peer(h, rank, (char*)h->xblock);
+  return RB_OK;
+}
+
+extern "C" size_t rb_bfs_xchg_handle_bytes(void) { return sizeof(cudaIpcMemHandle_t); }
+
+extern "C" int rb_bfs_xchg_handle(rb_bfs* h, void* out) {
+  if (!h || !h->xblock || !out) return rb_null_handle(__func__);
+  cudaIpcMemHandle_t m;
+  RB_CUDA_TRY(cudaIpcGetMemHandle(&m, h->xblock));
+  memcpy(out, &m, sizeof(m));
+  return RB_OK;
+}
+
+// handles: world IPC handles (rank order, rb_bfs_xchg_handle of every rank).
+extern "C" int rb_bfs_xchg_open(rb_bfs* h, const void* handles) {
+  if (!h || !h->xblock || !handles) return rb_null_handle(__func__);
+  for (int q = 0; q < h->x.world; ++q) {
+    if (q == h->x.rank) continue;
+    cudaIpcMemHandle_t m;
+    memcpy(&m, (const char*)handles + (size_t)q * sizeof(m), sizeof(m));
+    void* b = nullptr;
+    RB_CUDA_TRY(cudaIpcOpenMemHandle(&b, m, cudaIpcMemLazyEnablePeerAccess));
+    h->x_opened.push_back(b);
+    xparams_peer(h, q, (char*)b);
+  }
+  return RB_OK;
+}
+
+// One process, several engines (the emulation on one GPU): peers are plain pointers.
+extern "C" int rb_bfs_xchg_connect_local(rb_bfs* const* hs, int32_t world) {
+  if (!hs || world < 1 || world > kMaxWorld) return rb_null_handle(__func__);
+  for (int r = 0; r < world; ++r)
+    if (!hs[r] || !hs[r]->xblock || hs[r]->x.world != world || hs[r]->x.rank != r) return rb_null_handle(__func__);
+  for (int r = 0; r < world; ++r)
+    for (int q = 0; q < world; ++q) xparams_peer(hs[r], q, (char*)hs[q]->xblock);
+  return RB_OK;
+}
+
+// Per-root reset of a distributed traversal (engine.py:526-532): local state,
+// the exchange buffers (xg[0] = {source}), the source seeded by its owner.
+extern "C" int rb_bfs_dist_reset(rb_bfs* h, int64_t source_global, int64_t deg_source, void* stream) {
+  if (!h || !h->xblock || source_global < 0 || source_global >= h->n_glob) {
+    rb_set_error("rb_bfs_dist_reset: invalid argument (source %lld, n %lld)", (long long)source_global,
+                 (long long)h->n_glob);
+    return RB_ERR_ARG;
+  }
+  {
+    const cudaError_t prior = cudaGetLastError();
+    if (prior != cudaSuccess) {
+      rb_set_error("rb_bfs_dist_reset: pending CUDA error before the reset: %s", cudaGetErrorString(prior));
+      return RB_ERR_CUDA;
+    }
+  }
+  int rc = rb_bfs_reset_part(h, source_global, stream);
+  if (rc) return rc;
+  dist_reset_x<<<h->sms * 2, 256, 0, (cudaStream_t)stream>>>(h->x, source_global);
+  RB_CUDA_TRY(cudaGetLastError());
+  h->src_deg = deg_source;
+  return RB_OK;
+}
+
+static KParams dist_kparams(const rb_bfs* h) {
+  KParams kp = h->kp;
+  kp.level0 = 0;
+  kp.dir0 = 0;
+  kp.need_compact0 = 0;
+  kp.max_levels = kRecCap;
+  kp.nf0 = 1;
+  kp.mf0 = h->src_deg;
+  kp.mu0 = h->prm.m_directed - h->src_deg;
+  kp.m_directed = h->prm.m_directed;
+  kp.from_fin = 0;
+  kp.exec_opt = (h->exec_opt && h->prm.hybrid) ? 1 : 0;
+  kp.fcur_ext = nullptr;
+  kp.nzcur_ext = nullptr;
+  return kp;
+}
+
+static const void* dist_kernel(const rb_bfs* h, bool emu) {
+  const bool small = h->n_dev <= kSmallGraph;
+  if (emu) return small ? (const void*)bfs_dist_emu<true, 4> : (const void*)bfs_dist_emu<true, 8>;
+  return small ? (const void*)bfs_dist<true, 4> : (const void*)bfs_dist<true, 8>;
+}
+
+// The whole traversal of this rank: one persistent launch (every rank launches).
+extern "C" int rb_bfs_dist_traverse(rb_bfs* h, void* stream) {
+  if (!h || !h->xblock) return rb_null_handle(__func__);
+  cudaStream_t s = (cudaStream_t)stream;
+  KParams kp = dist_kparams(h);
+  XParams x = h->x;
+  void* args[] = {&kp, &x};
+  RB_CUDA_TRY(cudaEventRecord(h->ev_start, s));
+  cudaError_t e =
+      cudaLaunchCooperativeKernel(dist_kernel(h, false), dim3(h->blocks), dim3(kThreads), args, 0, s);
+  if (e != cudaSuccess) {
+    rb_set_error("distributed launch failed: %s", cudaGetErrorString(e));
+    return RB_ERR_CUDA;
+  }
+  RB_CUDA_TRY(cudaEventRecord(h->ev_end, s));
+  h->launched = true;
+  h->recs.clear();
+  return RB_OK;
+}
+
+// One GPU: all ranks' traversal in one cooperative launch (engines of one
+// process, rb_bfs_xchg_connect_local'ed, each reset with rb_bfs_dist_reset).
+extern "C" int rb_bfs_dist_traverse_emu(rb_bfs* const* hs, int32_t world, void* stream) {
+  if (!hs || world < 1 || world > kMaxWorld || !hs[0]) return rb_null_handle(__func__);
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<KParams> kps((size_t)world);
+  std::vector<XParams> xps((size_t)world);
+  for (int r = 0; r < world; ++r) {
+    kps[(size_t)r] = dist_kparams(hs[r]);
+    kps[(size_t)r].bar = hs[0]->kp.bar;  // one grid, one barrier counter
+    xps[(size_t)r] = hs[r]->x;
+  }
+  // (the parameter arrays live in rank 0's slot area tail: a small device scratch)
+  static thread_local void* scratch = nullptr;
+  static thread_local size_t scratch_bytes = 0;
+  const size_t need = (sizeof(KParams) + sizeof(XParams)) * (size_t)world;
+  if (scratch_bytes < need) {
+    if (scratch) cudaFree(scratch);
+    RB_CUDA_TRY(cudaMalloc(&scratch, need));
+    scratch_bytes = need;
+  }
+  RB_CUDA_TRY(cudaMemcpyAsync(scratch, kps.data(), sizeof(KParams) * world, cudaMemcpyHostToDevice, s));
+  RB_CUDA_TRY(cudaMemcpyAsync((char*)scratch + sizeof(KParams) * world, xps.data(), sizeof(XParams) * world,
+                              cudaMemcpyHostToDevice, s));
+  EmuParams ep{world, (const KParams*)scratch, (const XParams*)((char*)scratch + sizeof(KParams) * world)};
+  void* args[] = {&ep};
+  rb_bfs* h0 = hs[0];
+  RB_CUDA_TRY(cudaMemsetAsync(h0->kp.bar, 0, 64, s));
+  RB_CUDA_TRY(cudaEventRecord(h0->ev_start, s));
+  cudaError_t e =
+      cudaLaunchCooperativeKernel(dist_kernel(h0, true), dim3(h0->blocks), dim3(kThreads), args, 0, s);
+  if (e != cudaSuccess) {
+    rb_set_error("emulated distributed launch failed: %s", cudaGetErrorString(e));
+    return RB_ERR_CUDA;
+  }
+  RB_CUDA_TRY(cudaEventRecord(h0->ev_end, s));
+  RB_CUDA_TRY(cudaStreamSynchronize(s));  // (the parameter scratch is reused by the next call)
+  for (int r = 0; r < world; ++r) {
+    hs[r]->launched = true;
+    hs[r]->recs.clear();
+  }
+  return RB_OK;
+}
+
+// After a distributed traversal: level records (rank 0's engine holds them),
+// elapsed device time, and the cross-barrier count carried to the next launch.
+extern "C" int rb_bfs_dist_results(rb_bfs* h, rb_level_record* h_records, int64_t cap, int64_t* n_records,
+                                   double* elapsed_s, void* stream) {
+  if (!h || !h->xblock) return rb_null_handle(__func__);
+  cudaStream_t s = (cudaStream_t)stream;
+  Final f;
+  RB_CUDA_TRY(cudaMemcpyAsync(&f, h->kp.fin, sizeof(Final), cudaMemcpyDeviceToHost, s));
+  RB_CUDA_TRY(cudaStreamSynchronize(s));
+  if (f.nf > 0) {
+    rb_set_error("distributed traversal deeper than %lld levels", (long long)kRecCap);
+    return RB_ERR_CUDA;
+  }
+  h->x.xepoch0 = (uint32_t)f.pad;
+  h->launched = false;
+  const int64_t nr = f.levels_done;
+  if (h_records && nr > 0) {
+    std::vector<rb_level_record> tmp((size_t)nr);
+    RB_CUDA_TRY(cudaMemcpy(tmp.data(), h->kp.rec, (size_t)nr * sizeof(rb_level_record), cudaMemcpyDeviceToHost));
+    memcpy(h_records, tmp.data(), (size_t)(nr < cap ? nr : cap) * sizeof(rb_level_record));
+  }
+  if (n_records) *n_records = nr;
+  if (elapsed_s) {
+    float ms = 0.f;
+    RB_CUDA_TRY(cudaEventSynchronize(h->ev_end));
+    cudaEventElapsedTime(&ms, h->ev_start, h->ev_end);
+    *elapsed_s = 1e-3 * (double)ms;
   }
   return RB_OK;
 }

@@ -61,8 +61,8 @@ __device__ __forceinline__ uint64_t scramble(uint64_t x, const GenParams& g) {
   return x;
 }
 
-__global__ void kron_kernel(GenParams g, uint2* __restrict__ out) {
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < g.m; e += (int64_t)gridDim.x * blockDim.x) {
+__global__ void kron_kernel(GenParams g, int64_t e_lo, int64_t e_hi, uint2* __restrict__ out) {
+  for (int64_t e = e_lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < e_hi; e += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t chunk = (uint64_t)(e / kChunkEdges);
     const int64_t i = e % kChunkEdges;  // edge index inside the chunk
     uint64_t src = 0, dst = 0;
@@ -85,7 +85,7 @@ __global__ void kron_kernel(GenParams g, uint2* __restrict__ out) {
       src = (src << 1) | (uint64_t)((q >> 1) & 1);
       dst = (dst << 1) | (uint64_t)(q & 1);
     }
-    out[e] = make_uint2((uint32_t)scramble(src, g), (uint32_t)scramble(dst, g));
+    out[e - e_lo] = make_uint2((uint32_t)scramble(src, g), (uint32_t)scramble(dst, g));
   }
 }
 
@@ -131,9 +131,10 @@ uint64_t splitmix64(uint64_t x) {
 
 }  // namespace
 
-extern "C" int rb_kronecker_generate(int scale, int64_t edgefactor, uint64_t seed, double a, double b, double c,
-                                     uint32_t* d_edges, void* stream) {
-  if (scale < 1 || scale > 30 || edgefactor < 1 || !d_edges) {
+extern "C" int rb_kronecker_generate_range(int scale, int64_t edgefactor, uint64_t seed, double a, double b,
+                                           double c, int64_t e_lo, int64_t e_hi, uint32_t* d_edges, void* stream) {
+  if (scale < 1 || scale > 30 || edgefactor < 1 || (!d_edges && e_hi > e_lo) || e_lo < 0 ||
+      e_hi > ((int64_t)1 << scale) * edgefactor || e_hi < e_lo) {
     rb_set_error("rb_kronecker_generate: invalid argument");
     return RB_ERR_ARG;
   }
@@ -157,11 +158,22 @@ extern "C" int rb_kronecker_generate(int scale, int64_t edgefactor, uint64_t see
     g.shift[r] = shifts[r];
   }
   cudaStream_t s = (cudaStream_t)stream;
-  int64_t blocks = (g.m + 255) / 256;
+  if (e_hi == e_lo) return RB_OK;
+  int64_t blocks = (e_hi - e_lo + 255) / 256;
   if (blocks > 148 * 64) blocks = 148 * 64;
-  kron_kernel<<<(int)blocks, 256, 0, s>>>(g, reinterpret_cast<uint2*>(d_edges));
+  kron_kernel<<<(int)blocks, 256, 0, s>>>(g, e_lo, e_hi, reinterpret_cast<uint2*>(d_edges));
   RB_CUDA_TRY(cudaGetLastError());
   return RB_OK;
+}
+
+extern "C" int rb_kronecker_generate(int scale, int64_t edgefactor, uint64_t seed, double a, double b, double c,
+                                     uint32_t* d_edges, void* stream) {
+  if (scale < 1 || scale > 30 || edgefactor < 1 || !d_edges) {
+    rb_set_error("rb_kronecker_generate: invalid argument");
+    return RB_ERR_ARG;
+  }
+  return rb_kronecker_generate_range(scale, edgefactor, seed, a, b, c, 0, ((int64_t)1 << scale) * edgefactor, d_edges,
+                                     stream);
 }
 
 extern "C" size_t rb_chunglu_workspace_bytes(int64_t n) {

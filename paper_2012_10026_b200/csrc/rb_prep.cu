@@ -944,3 +944,119 @@ extern "C" int rb_transpose_rows(const int64_t* d_rs, const int32_t* d_col, int6
   RB_CUDA_TRY(cudaGetLastError());
   return RB_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Sharded CSR build / relabel building blocks (configs[3]: the graph is split
+// over the ranks by vertex block; see paper_2012_10026_b200/sharded.py)
+
+namespace {
+__global__ void relabel_keys(const int64_t* __restrict__ rs, const int32_t* __restrict__ col, int64_t n_local,
+                             int64_t v_lo, const uint32_t* __restrict__ inv, uint64_t* __restrict__ keys) {
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t base = rs[0];
+  for (int64_t v = warp; v < n_local; v += nwarps) {
+    const uint64_t nv = inv[v_lo + v];
+    for (int64_t j = rs[v] + lane; j < rs[v + 1]; j += 32) keys[j - base] = (nv << 32) | inv[col[j]];
+  }
+}
+
+__global__ void keys_rows(const uint64_t* __restrict__ keys, int64_t m, int64_t v_lo, int64_t n_local,
+                          int64_t* __restrict__ rs, int32_t* __restrict__ col) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= m; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = (i < m) ? (int64_t)(keys[i] >> 32) - v_lo : n_local;
+    const int64_t ps = (i > 0) ? (int64_t)(keys[i - 1] >> 32) - v_lo : -1;
+    for (int64_t v = ps + 1; v <= s; ++v) rs[v] = i;
+    if (i < m) col[i] = (int32_t)(keys[i] & 0xffffffffu);
+  }
+}
+}  // namespace
+
+// The sorted unique keys (u << 32 | v) rb_csr_build left in its workspace.
+extern "C" int rb_csr_keys(const void* d_ws, const uint64_t** d_keys, int64_t* m_directed) {
+  if (!d_ws || !d_keys || !m_directed) {
+    rb_set_error("rb_csr_keys: invalid argument");
+    return RB_ERR_ARG;
+  }
+  CsrHeader hdr;
+  RB_CUDA_TRY(cudaMemcpy(&hdr, d_ws, sizeof(hdr), cudaMemcpyDeviceToHost));
+  *d_keys = (const uint64_t*)((const char*)d_ws + hdr.result_off);
+  *m_directed = hdr.m_directed;
+  return RB_OK;
+}
+
+extern "C" size_t rb_keys_workspace_bytes(int64_t m) {
+  size_t t1 = 0, t2 = 0;
+  const int64_t k = m > 0 ? m : 1;
+  cub::DoubleBuffer<uint64_t> db(nullptr, nullptr);
+  cub::DeviceRadixSort::SortKeys(nullptr, t1, db, k, 0, 64);
+  cub::DeviceSelect::Unique(nullptr, t2, (uint64_t*)nullptr, (uint64_t*)nullptr, (int64_t*)nullptr, k);
+  return (size_t)k * 8 + 256 + std::max(t1, t2) + 256;
+}
+
+// Sort keys[0, m) (low end_bit bits significant) and drop duplicates, in place.
+extern "C" int rb_keys_sort_unique(uint64_t* d_keys, int64_t m, int end_bit, void* d_ws, size_t ws_bytes,
+                                   int64_t* m_out, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (m < 0 || !m_out || end_bit < 1 || end_bit > 64 || (m > 0 && (!d_keys || ws_bytes < rb_keys_workspace_bytes(m)))) {
+    rb_set_error("rb_keys_sort_unique: invalid argument");
+    return RB_ERR_ARG;
+  }
+  *m_out = 0;
+  if (m == 0) return RB_OK;
+  Carver c(d_ws, ws_bytes);
+  uint64_t* alt = c.take<uint64_t>((size_t)m);
+  int64_t* nsel = c.take<int64_t>(1);
+  size_t t1 = 0, t2 = 0;
+  cub::DoubleBuffer<uint64_t> db(d_keys, alt);
+  cub::DeviceRadixSort::SortKeys(nullptr, t1, db, m, 0, end_bit);
+  cub::DeviceSelect::Unique(nullptr, t2, (uint64_t*)nullptr, (uint64_t*)nullptr, (int64_t*)nullptr, m);
+  size_t tb = std::max(t1, t2);
+  void* temp = c.take<char>(tb);
+  RB_CUDA_TRY(cub::DeviceRadixSort::SortKeys(temp, tb, db, m, 0, end_bit, s));
+  tb = std::max(t1, t2);
+  uint64_t* sorted = db.Current();
+  uint64_t* out = sorted == d_keys ? alt : d_keys;
+  RB_CUDA_TRY(cub::DeviceSelect::Unique(temp, tb, sorted, out, nsel, m, s));
+  int64_t nu = 0;
+  RB_CUDA_TRY(cudaMemcpyAsync(&nu, nsel, 8, cudaMemcpyDeviceToHost, s));
+  RB_CUDA_TRY(cudaStreamSynchronize(s));
+  if (out != d_keys) RB_CUDA_TRY(cudaMemcpyAsync(d_keys, out, (size_t)nu * 8, cudaMemcpyDeviceToDevice, s));
+  *m_out = nu;
+  return RB_OK;
+}
+
+// Local CSR of the vertex block [v_lo, v_lo + n_local) from its sorted unique
+// keys (u << 32 | v): row starts (n_local + 1), columns (global ids), degrees.
+extern "C" int rb_keys_to_csr(const uint64_t* d_keys, int64_t m, int64_t v_lo, int64_t n_local, int64_t* d_rs,
+                              int32_t* d_col, int32_t* d_deg, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (m < 0 || n_local < 0 || v_lo < 0 || !d_rs || (n_local > 0 && !d_deg)) {
+    rb_set_error("rb_keys_to_csr: invalid argument");
+    return RB_ERR_ARG;
+  }
+  if (m == 0) {
+    RB_CUDA_TRY(cudaMemsetAsync(d_rs, 0, (size_t)(n_local + 1) * 8, s));
+  } else {
+    keys_rows<<<grid_for(m + 1), 256, 0, s>>>(d_keys, m, v_lo, n_local, d_rs, d_col);
+    RB_CUDA_TRY(cudaGetLastError());
+  }
+  if (n_local > 0) degrees_from_rs<<<grid_for(n_local), 256, 0, s>>>(d_rs, n_local, d_deg);
+  RB_CUDA_TRY(cudaGetLastError());
+  return RB_OK;
+}
+
+// Keys (inv[v] << 32 | inv[w]) of every entry of a local block's rows: the
+// relabelled graph, ready to be routed to the owners of the new ids.
+extern "C" int rb_relabel_keys(const int64_t* d_rs, const int32_t* d_col, int64_t n_local, int64_t v_lo,
+                               const uint32_t* d_inv, uint64_t* d_keys, void* stream) {
+  if (n_local < 0 || !d_rs || !d_inv || !d_keys) {
+    rb_set_error("rb_relabel_keys: invalid argument");
+    return RB_ERR_ARG;
+  }
+  if (n_local == 0) return RB_OK;
+  relabel_keys<<<grid_for(n_local * 32), 256, 0, (cudaStream_t)stream>>>(d_rs, d_col, n_local, v_lo, d_inv, d_keys);
+  RB_CUDA_TRY(cudaGetLastError());
+  return RB_OK;
+}

@@ -171,12 +171,14 @@ class GpuLocalLevel:
     """The local step of one rank: an rb_bfs engine created with a partition."""
 
     def __init__(self, g, bounds: list[int], rank: int, alpha: int, beta: int, hybrid: bool = True,
-                 record_levels: bool = False):
+                 record_levels: bool = False, rows=None):
+        """``g``: the whole RCM graph (every rank slices its block), or None
+        with ``rows`` = this rank's block (sharded.LocalRows, new ids) and
+        ``g`` replaced by (n, m_directed) for the policy."""
         torch = _lib.require_cuda()
         self.torch = torch
         self.device = torch.device("cuda", torch.cuda.current_device())
         L = _lib.lib()
-        rs, col, deg = g.device_arrays()
         lo, hi = bounds[rank], bounds[rank + 1]
         self.lo, self.hi = lo, hi
         n_glob = bounds[-1]
@@ -185,13 +187,23 @@ class GpuLocalLevel:
         s = _lib.stream_ptr()
         self._empty = torch.zeros(32, dtype=torch.int32, device=self.device)
         self.n_words_local = 0
+        if rows is None:
+            n_policy, m_directed = g.n, g.m_directed
+        else:
+            n_policy, m_directed = g
         if n_local == 0:
             self.h = None
             return
-        e0, e1 = int(rs[lo].item()), int(rs[hi].item())
-        self.rs_local = (rs[lo : hi + 1] - e0).contiguous()
-        self.col_local = col[e0:e1]
-        self.deg_local = deg[lo:hi].contiguous()
+        if rows is None:
+            rs, col, deg = g.device_arrays()
+            e0, e1 = int(rs[lo].item()), int(rs[hi].item())
+            self.rs_local = (rs[lo : hi + 1] - e0).contiguous()
+            self.col_local = col[e0:e1]
+            self.deg_local = deg[lo:hi].contiguous()
+        else:
+            assert (rows.lo, rows.hi) == (lo, hi), "rows do not match the partition bounds"
+            self.rs_local, self.col_local, self.deg_local = rows.rs, rows.col, rows.deg
+            e0, e1 = 0, rows.m_local
         m_local = e1 - e0
         # transpose slice: owned neighbours of every global vertex
         ws_bytes = L.rb_transpose_workspace_bytes(m_local, n_glob)
@@ -208,7 +220,7 @@ class GpuLocalLevel:
         flags[:n_local] = (self.deg_local == 0).to(torch.int64)
         words = (flags.view(nw, 32) << torch.arange(32, device=self.device, dtype=torch.int64)).sum(dim=1)
         self.iso = torch.where(words >= (1 << 31), words - (1 << 32), words).to(torch.int32)
-        prm = _lib.BfsParamsC(alpha, beta, int(hybrid), 1, g.n, g.m_directed, int(record_levels), 0)
+        prm = _lib.BfsParamsC(alpha, beta, int(hybrid), 1, n_policy, m_directed, int(record_levels), 0)
         part = _lib.PartitionC(lo, n_glob, _lib.ptr(self.td_rs).value, _lib.ptr(self.td_col).value)
         self.h = ctypes.c_void_p(0)
         _lib.check(L.rb_bfs_create_part(_lib.ptr(self.rs_local), _lib.ptr(self.col_local), _lib.ptr(self.col_local),
@@ -258,3 +270,117 @@ class GpuLocalLevel:
         if not self.h:
             return self.torch.empty(0, dtype=self.torch.int32, device=self.device)
         return _ptr_view(_lib.lib().rb_bfs_level_ptr(self.h), self.n_local)
+
+
+# ---------------------------------------------------------------------------
+# The exchange on the device: one persistent launch per rank per root
+# (rb_bfs.cu bfs_dist).  Each rank stores its next-frontier words and level
+# counters straight into every rank's buffers (CUDA IPC mappings over NVLink)
+# and meets the others at a system-scope barrier -- no host round trip and no
+# NCCL call per level.  On one GPU the ranks run as ONE cooperative launch over
+# all their data (bfs_dist_emu), the way the profiling guide asks multi-rank
+# kernels that wait on each other to be tested with fewer GPUs than ranks.
+
+
+class DevicePartition:
+    """One rank's engine (owned rows + transpose slice, GpuLocalLevel) plus its
+    exchange buffers: three global frontier bitmaps + summaries, the counter
+    slots and the cross-rank barrier counter, in one IPC-exportable block."""
+
+    def __init__(self, g, bounds: list[int], rank: int, world: int, alpha: int = 64, beta: int = 8,
+                 hybrid: bool = True, record_levels: bool = False, rows=None):
+        if any(bounds[r + 1] <= bounds[r] for r in range(world)):
+            raise ValueError(f"every rank needs a non-empty vertex block, got bounds {bounds}")
+        self.local = GpuLocalLevel(g, bounds, rank, alpha, beta, hybrid, record_levels, rows=rows)
+        self.rank, self.world = rank, world
+        self.bounds = bounds
+        self.g = g
+        _lib.check(_lib.lib().rb_bfs_xchg_alloc(self.local.h, world, rank), "rb_bfs_xchg_alloc")
+
+    @property
+    def h(self):
+        return self.local.h
+
+    def handle(self) -> bytes:
+        L = _lib.lib()
+        buf = (ctypes.c_char * int(L.rb_bfs_xchg_handle_bytes()))()
+        _lib.check(L.rb_bfs_xchg_handle(self.h, buf), "rb_bfs_xchg_handle")
+        return bytes(buf)
+
+    def open(self, handles: list[bytes]) -> None:
+        blob = b"".join(handles)
+        _lib.check(_lib.lib().rb_bfs_xchg_open(self.h, ctypes.c_char_p(blob)), "rb_bfs_xchg_open")
+
+    def reset(self, source: int, deg_source: int) -> None:
+        _lib.check(_lib.lib().rb_bfs_dist_reset(self.h, int(source), int(deg_source), _lib.stream_ptr()),
+                   "rb_bfs_dist_reset")
+
+    def traverse(self) -> None:
+        _lib.check(_lib.lib().rb_bfs_dist_traverse(self.h, _lib.stream_ptr()), "rb_bfs_dist_traverse")
+
+    def results(self):
+        """(records [DistRecord], executed directions, device seconds) of the
+        last traversal; the records are rank 0's (identical on every rank)."""
+        recs = (_lib.LevelRecordC * 4096)()
+        nrec = ctypes.c_int64(0)
+        el = ctypes.c_double(0.0)
+        _lib.check(_lib.lib().rb_bfs_dist_results(self.h, recs, len(recs), ctypes.byref(nrec), ctypes.byref(el),
+                                                  _lib.stream_ptr()), "rb_bfs_dist_results")
+        out = [DistRecord(int(r.level), int(r.direction), int(r.n_f), int(r.m_f), int(r.m_u), int(r.scanned_edges))
+               for r in recs[: nrec.value]]
+        return out, [int(r.reserved) for r in recs[: nrec.value]], el.value
+
+    def close(self) -> None:
+        self.local.close()
+
+
+def connect_emulated(parts: list[DevicePartition]) -> None:
+    """One process, one GPU: every rank's peers are the other engines' buffers."""
+    arr = (ctypes.c_void_p * len(parts))(*[p.h.value for p in parts])
+    _lib.check(_lib.lib().rb_bfs_xchg_connect_local(arr, len(parts)), "rb_bfs_xchg_connect_local")
+
+
+def run_emulated(parts: list[DevicePartition], source: int, deg_source: int):
+    """All ranks' traversal of one root in ONE cooperative launch on this GPU;
+    returns rank 0's (records, executed directions, device seconds)."""
+    for p in parts:
+        p.reset(source, deg_source)
+    arr = (ctypes.c_void_p * len(parts))(*[p.h.value for p in parts])
+    _lib.check(_lib.lib().rb_bfs_dist_traverse_emu(arr, len(parts), _lib.stream_ptr()), "rb_bfs_dist_traverse_emu")
+    res = parts[0].results()
+    for p in parts[1:]:
+        p.results()  # (clears the launched state of every engine)
+    return res
+
+
+class DeviceExchangeBfs:
+    """Multi-process driver (one rank per GPU): IPC handles are exchanged once
+    through torch.distributed, then every root is reset + ONE launch per rank."""
+
+    def __init__(self, g, bounds: list[int], rank: int, world: int, alpha: int = 64, beta: int = 8,
+                 hybrid: bool = True, record_levels: bool = False, group=None, rows=None):
+        import torch.distributed as dist
+
+        self.part = DevicePartition(g, bounds, rank, world, alpha, beta, hybrid, record_levels, rows=rows)
+        handles = [None] * world
+        dist.all_gather_object(handles, self.part.handle(), group=group)
+        self.part.open(handles)
+        dist.barrier(group=group)
+
+    @property
+    def local(self):
+        return self.part.local
+
+    def run(self, source: int, deg_source: int):
+        self.part.reset(source, deg_source)
+        self.part.traverse()
+        recs, _, _ = self.part.results()
+        return recs
+
+    def elapsed(self) -> float:
+        el = ctypes.c_double(0.0)
+        _lib.check(_lib.lib().rb_bfs_elapsed(self.part.h, ctypes.byref(el)), "rb_bfs_elapsed")
+        return el.value
+
+    def close(self):
+        self.part.close()

@@ -166,3 +166,16 @@ def test_result_pool_never_hands_out_a_live_buffer():
     gc.collect()
     c = engine.fresh_int32(n)  # now a pooled (warm) mapping may come back
     assert c.flags.writeable and c.size == n and c.dtype == np.int32
+
+
+def test_s29_memory_plan_fits_b200():
+    """configs[3] dry run: every stage of the sharded scale-29 pipeline fits one
+    B200's HBM at 8 GPUs (sharded.memory_plan), and would not at 2."""
+    from paper_2012_10026_b200.sharded import memory_plan, owner_bounds
+
+    plan = memory_plan(29, 8)
+    assert plan["fits"], plan
+    assert plan["stages_gb"]["rcm_on_root"] == max(plan["stages_gb"].values())
+    assert not memory_plan(29, 2)["fits"] or memory_plan(29, 2)["peak_gb"] > 100
+    b = owner_bounds(1 << 29, 8)
+    assert b[0] == 0 and b[-1] == 1 << 29 and all(x % 8192 == 0 for x in b[:-1]) and len(b) == 9
