@@ -30,6 +30,11 @@ int rb_version(void);
 int rb_kronecker_generate(int scale, int64_t edgefactor, uint64_t seed, double a, double b, double c,
                           uint32_t* d_edges, void* stream);
 
+/* Edges [e_lo, e_hi) of the same stream (the sharded scale-29 build: each
+ * rank draws its share of the 65,536-edge chunks). */
+int rb_kronecker_generate_range(int scale, int64_t edgefactor, uint64_t seed, double a, double b, double c,
+                                int64_t e_lo, int64_t e_hi, uint32_t* d_edges, void* stream);
+
 /* Chung-Lu power-law graph (BASELINE configs[4]; no reference generator --
  * recipe in paper_2012_10026_b200/generator.py).  d_weights: n positive
  * int64 integer weights; writes m_pairs (u,v) uint32 pairs, each endpoint
@@ -52,6 +57,24 @@ int rb_csr_build(const uint32_t* d_edges, int64_t m_raw, int64_t n, void* d_ws, 
  * int32, degrees n int32). */
 int rb_csr_emit(const void* d_ws, int64_t m_directed, int64_t n, int64_t* d_row_starts,
                 int32_t* d_col, int32_t* d_degrees, void* stream);
+
+/* Sharded build / relabel (configs[3], paper_2012_10026_b200/sharded.py):
+ * rb_csr_keys: the sorted unique keys (u << 32 | v) rb_csr_build left in its
+ * workspace (what a rank routes to the owners of u);
+ * rb_keys_sort_unique: sort keys[0, m) on the low end_bit bits and drop
+ * duplicates in place (workspace rb_keys_workspace_bytes(m));
+ * rb_keys_to_csr: CSR rows of the vertex block [v_lo, v_lo + n_local) from
+ * its sorted unique keys (row starts from 0, global column ids, degrees);
+ * rb_relabel_keys: keys inv[v] << 32 | inv[w] of a block's rows (its part of
+ * apply_permutation, to be routed to the owners of the new ids). */
+int rb_csr_keys(const void* d_ws, const uint64_t** d_keys, int64_t* m_directed);
+size_t rb_keys_workspace_bytes(int64_t m);
+int rb_keys_sort_unique(uint64_t* d_keys, int64_t m, int end_bit, void* d_ws, size_t ws_bytes, int64_t* m_out,
+                        void* stream);
+int rb_keys_to_csr(const uint64_t* d_keys, int64_t m, int64_t v_lo, int64_t n_local, int64_t* d_row_starts,
+                   int32_t* d_col, int32_t* d_degrees, void* stream);
+int rb_relabel_keys(const int64_t* d_row_starts, const int32_t* d_col, int64_t n_local, int64_t v_lo,
+                    const uint32_t* d_inv, uint64_t* d_keys, void* stream);
 
 /* ---- RCM: replaces reorder.py:198-237 (rcm / _rcm_impl / _rcm_walk) ----- */
 /* Outputs perm (new->old) and inv (old->new), |V+|, component ranges (pairs of
