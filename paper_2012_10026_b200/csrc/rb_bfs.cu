@@ -3149,10 +3149,10 @@ extern "C" int rb_bfs_dist_results(rb_bfs* h, rb_level_record* h_records, int64_
     memcpy(h_records, tmp.data(), (size_t)(nr < cap ? nr : cap) * sizeof(rb_level_record));
   }
   if (n_records) *n_records = nr;
-  if (elapsed_s) {
+  if (elapsed_s) {  // (emulation: only the first rank's engine recorded the launch events)
     float ms = 0.f;
     RB_CUDA_TRY(cudaEventSynchronize(h->ev_end));
-    cudaEventElapsedTime(&ms, h->ev_start, h->ev_end);
+    RB_CUDA_TRY(cudaEventElapsedTime(&ms, h->ev_start, h->ev_end));
     *elapsed_s = 1e-3 * (double)ms;
   }
   return RB_OK;

@@ -318,14 +318,16 @@ class DevicePartition:
     def traverse(self) -> None:
         _lib.check(_lib.lib().rb_bfs_dist_traverse(self.h, _lib.stream_ptr()), "rb_bfs_dist_traverse")
 
-    def results(self):
+    def results(self, timed: bool = True):
         """(records [DistRecord], executed directions, device seconds) of the
-        last traversal; the records are rank 0's (identical on every rank)."""
+        last traversal; the records are rank 0's (identical on every rank).
+        ``timed=False``: the engine did not record the launch (emulated ranks > 0)."""
         recs = (_lib.LevelRecordC * 4096)()
         nrec = ctypes.c_int64(0)
         el = ctypes.c_double(0.0)
-        _lib.check(_lib.lib().rb_bfs_dist_results(self.h, recs, len(recs), ctypes.byref(nrec), ctypes.byref(el),
-                                                  _lib.stream_ptr()), "rb_bfs_dist_results")
+        _lib.check(_lib.lib().rb_bfs_dist_results(self.h, recs, len(recs), ctypes.byref(nrec),
+                                                  ctypes.byref(el) if timed else None, _lib.stream_ptr()),
+                   "rb_bfs_dist_results")
         out = [DistRecord(int(r.level), int(r.direction), int(r.n_f), int(r.m_f), int(r.m_u), int(r.scanned_edges))
                for r in recs[: nrec.value]]
         return out, [int(r.reserved) for r in recs[: nrec.value]], el.value
@@ -349,7 +351,7 @@ def run_emulated(parts: list[DevicePartition], source: int, deg_source: int):
     _lib.check(_lib.lib().rb_bfs_dist_traverse_emu(arr, len(parts), _lib.stream_ptr()), "rb_bfs_dist_traverse_emu")
     res = parts[0].results()
     for p in parts[1:]:
-        p.results()  # (clears the launched state of every engine)
+        p.results(timed=False)  # (clears the launched state of every engine)
     return res
 
 
