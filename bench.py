@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: shard the 64 independent roots over per-GPU graph replicas (throughput mode). "
                          "Default: ONE traversal per root over the 1D vertex-block partition of all GPUs")
+    ap.add_argument("--partitioned", action="store_true",
+                    help="force the 1D-partition path (device-side exchange) also at one GPU (loopback check)")
     ap.add_argument("--validate-roots", type=int, default=N_ROOTS,
                     help="validate this many roots' trees on the GPU (outside the timed region)")
     a = ap.parse_args()
@@ -403,16 +405,21 @@ def run_ours(args):
         local = 0
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    if world > 1 or args.partitioned:
         import torch.distributed as dist
 
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         if one_gpu:
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     g2, stats, roots, raw, prep = build_graph(args, rb, torch)
-    if world > 1 and not args.replicas:
+    if (world > 1 and not args.replicas) or args.partitioned:
         return run_partitioned(args, rb, torch, dist, g2, stats, roots, raw, world, rank, prep)
 
     eng = rb.BfsEngine(g2, rb.BfsParams(mode=args.mode))
@@ -565,85 +572,75 @@ def cpu_baseline_sample(g2, roots, raw, seconds):
 
 def run_partitioned(args, rb, torch, dist, g2, stats, roots, raw, world, rank, prep):
     """--gpus N > 1: ONE traversal per root over the 1D vertex-block partition
-    (distributed.py): per level a local step per GPU + NCCL counter all-reduce
-    and frontier-bitmap all-gather.  Per-root time = max over ranks (device
-    events), value = harmonic mean over roots (strong scaling: same graph,
-    same roots)."""
-    from paper_2012_10026_b200.distributed import GpuLocalLevel, PartitionedBfs, partition_bounds
+    of all GPUs with the exchange on the device (distributed.DeviceExchangeBfs:
+    one persistent launch per rank per root; next-frontier words and counters
+    stored into every peer's buffers over NVLink, a system-scope barrier per
+    level).  Per-root time = max over ranks of the device event time; value =
+    harmonic mean over the 64 roots (strong scaling: same graph, same roots)."""
+    from paper_2012_10026_b200.distributed import DeviceExchangeBfs, partition_bounds
 
     n_plus = stats.n_non_isolated
-    rs_host = g2.row_starts
     deg_host = g2.degrees
-    bounds = partition_bounds(rs_host, n_plus, world)
-    local = GpuLocalLevel(g2, bounds, rank, alpha=64, beta=8, hybrid=args.mode != "level_sync")
-    drv = PartitionedBfs(local, bounds, rank, world, n_policy=g2.n, m_directed=g2.m_directed,
-                         hybrid=args.mode != "level_sync")
+    bounds = partition_bounds(g2.row_starts, n_plus, world)
+    drv = DeviceExchangeBfs(g2, bounds, rank, world, hybrid=args.mode != "level_sync")
     my = list(range(N_ROOTS)) if not args.profile_roots else list(range(args.profile_roots))
     sweeps = 1 if args.profile_roots else args.steps
-    for i in range(args.warmup):
+    for _ in range(args.warmup):
         for j in my:
             drv.run(int(roots[j]), int(deg_host[roots[j]]))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    ev_a = torch.cuda.Event(enable_timing=True)
-    ev_b = torch.cuda.Event(enable_timing=True)
-    times, teps, alg, nlev = [], [], [], []
+    t_root = {j: [] for j in my}
+    recs_of = {}
     dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
-        for j in [j for _ in range(sweeps) for j in my]:
-            flush.zero_()
-            dist.barrier()
-            torch.cuda.synchronize()
-            ev_a.record()
-            recs = drv.run(int(roots[j]), int(deg_host[roots[j]]))
-            ev_b.record()
-            torch.cuda.synchronize()
-            t = torch.tensor([ev_a.elapsed_time(ev_b) / 1e3], dtype=torch.float64, device=drv.local.device)
-            if drv.stage:
-                t = t.cpu()
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            el = float(t.item())
-            times.append(el)
-            teps.append(raw[j] / el)
-            levels = [type("R", (), dict(direction="top_down" if r.direction == 0 else "bottom_up", n_f=r.n_f,
-                                         scanned_edges=r.scanned))() for r in recs]
-            alg.append(algorithmic_bytes(levels, n_plus, n_plus))
-            nlev.append(len(recs))
-    # e2e: the same traversal + each rank's parent slice copied to host
+        for _ in range(sweeps):
+            for j in my:
+                flush.zero_()
+                recs_of[j] = drv.run(int(roots[j]), int(deg_host[roots[j]]))
+                t_root[j].append(drv.elapsed())
+    dist.barrier()
+    loc = np.array([float(np.mean(t_root[j])) for j in my], np.float64)
+    t = torch.from_numpy(loc).cuda()
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)  # the root's time = its slowest rank
+    times = t.cpu().numpy()
+    teps = [raw[j] / times[i] for i, j in enumerate(my)]
+    # e2e: the same traversal + every rank's parent block copied to its host
     e2e = []
-    for j in my[: min(len(my), 8)]:
+    for j in my[: min(len(my), 16)]:
         dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         drv.run(int(roots[j]), int(deg_host[roots[j]]))
-        _ = local.parents().cpu().numpy()
-        t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64)
-        if not drv.stage:
-            t = t.cuda()
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e.append(raw[j] / float(t.item()))
+        _ = drv.local.parents().cpu().numpy()
+        tt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e.append(raw[j] / float(tt.item()))
     if rank == 0:
         peak, peak_kind = measured_peak()
+        alg = [algorithmic_bytes([type("R", (), dict(direction="top_down" if r.direction == 0 else "bottom_up",
+                                                       n_f=r.n_f, scanned_edges=r.scanned))() for r in recs_of[j]],
+                                 n_plus, n_plus) for j in my]
         ach = float(np.sum(alg) / np.sum(times) / 1e9) / world  # per GPU
         line = {
             "metric": METRIC, "value": hmean(teps) / 1e9, "unit": UNIT, "n_gpus": world, "steps": sweeps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * float(np.sum(times)) / sweeps, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": 1e3 * float(np.sum(times)), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int32",
             "data": workload(args)[1] + ", built on device",
-            "config": {"workload": workload(args)[0], "scale": args.scale,
-                       "edgefactor": args.edgefactor, "roots": len(my), "mode": args.mode,
-                       "parallelism": f"1d-partition x{world} (NCCL all-gather / all-reduce per level)",
+            "config": {"workload": workload(args)[0], "scale": args.scale, "edgefactor": args.edgefactor,
+                       "roots": len(my), "step": f"one sweep of the {len(my)} seeded roots", "mode": args.mode,
+                       "parallelism": f"1d-partition x{world} (device-side exchange over NVLink peer memory)",
                        "partition_bounds": bounds, "l2": "flushed (256 MiB write) before every root"},
             "preprocessing_s": prep,
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                         "peak_kind": peak_kind, "kernel": "bfs_persistent (per GPU)", "traffic": None},
-            "e2e": {"value": hmean(e2e) / 1e9, "unit": UNIT, "h2d_bytes_per_step": 8,
-                    "d2h_bytes_per_step": int(4 * (bounds[1] - bounds[0]))},
-            "gpu_launches": int(sum(2 * x + 1 for x in nlev)),  # per root: seed + per level (step + summary)
+                         "peak_kind": peak_kind, "kernel": "bfs_dist (per GPU)", "traffic": None},
+            "e2e": {"value": hmean(e2e) / 1e9, "unit": UNIT, "h2d_bytes_per_step": 8 * N_ROOTS,
+                    "d2h_bytes_per_step": int(4 * (bounds[1] - bounds[0])) * N_ROOTS},
+            "gpu_launches": int(sweeps * len(my) * 3),  # reset + exchange reset + bfs_dist per root
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
-    local.close()
+    drv.close()
     dist.destroy_process_group()
 
 

@@ -792,6 +792,16 @@ __device__ __forceinline__ int32_t bu_heavy(const KParams& p, const uint32_t* fc
   return -1;
 }
 
+// Offset in a bottom-up warp step (KB words) of lane l's k-th vertex: lane l
+// owns bit l of every word, so each of the step's loads is one coalesced
+// warp access.  (Measured and rejected: lane l owning KB consecutive
+// vertices with 16-byte loads -- s26 bottom-up 265 -> 311 us/root, four times
+// the L1 wavefronts.)
+template <int KB>
+__device__ __forceinline__ uint32_t step_off_t(uint32_t lane, uint32_t k) {
+  return (k << 5) | lane;
+}
+
 template <bool kRev, int KB, bool kCollect>
 RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uint32_t* fnext, uint8_t* nznext,
                          Acc& acc, uint32_t* s_found, uint32_t* s_pair, uint32_t* s_next, uint32_t* ulist,
@@ -799,6 +809,7 @@ RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uin
   const uint32_t lane = rb::lane_id();
   const uint64_t nw = (uint64_t)p.n_words;
   int32_t* const level_out = p.level;
+  auto step_off = [](uint32_t l, uint32_t k) { return step_off_t<KB>(l, k); };
   // CTA b owns the steps b, b + gridDim.x, ... (KB words each); its warps
   // take them in order from a shared-memory counter, so a warp that meets
   // long rows does not hold up the CTA.  Software pipeline: the next step
@@ -980,14 +991,14 @@ RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uin
     uint32_t foundm = 0, needm = 0, checks = 0, dsum = 0, dmax = 0, h0m = 0;
     int32_t* const par_out = p.parent + vbase;
 #pragma unroll
-    for (int k = 0; k < KB; ++k) {
+    for (int k = 0; k < KB; ++k) {  // (inactive vertices hold hv = -1: no hit)
       const bool act = (actm >> k) & 1u;
-      const bool h0 = act && hv[k].x >= 0 && ((hb0[k] >> (hv[k].x & 31)) & 1u);
-      const bool h1 = act && !h0 && hv[k].y >= 0 && ((hb1[k] >> (hv[k].y & 31)) & 1u);
+      const bool h0 = hv[k].x >= 0 && ((hb0[k] >> (hv[k].x & 31)) & 1u);
+      const bool h1 = !h0 && hv[k].y >= 0 && ((hb1[k] >> (hv[k].y & 31)) & 1u);
       const bool found = h0 || h1;
       h0m += h0 ? 1u : 0u;
       checks += act ? (h0 ? 1u : min(dg[k], 2u)) : 0u;  // (a second-neighbour hit implies dg >= 2)
-      if (found) par_out[32 * k] = h0 ? hv[k].x : hv[k].y;
+      rb::st_if(par_out + 32 * k, h0 ? hv[k].x : hv[k].y, found);  // predicated store, no branch
       foundm |= (uint32_t)found << k;
       needm |= (uint32_t)(act && !found && dg[k] > 2u) << k;
       dsum += found ? dg[k] : 0u;
@@ -996,8 +1007,7 @@ RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uin
     constexpr int kFirst = 2;
     if (foundm && level_out) {
 #pragma unroll
-      for (int k = 0; k < KB; ++k)
-        if ((foundm >> k) & 1u) level_out[vbase + 32 * k] = (int32_t)(L + 1);
+      for (int k = 0; k < KB; ++k) rb::st_if(level_out + vbase + 32 * k, (int32_t)(L + 1), (foundm >> k) & 1u);
     }
     acc.n += __popc(foundm);
     acc.deg += dsum;
@@ -1006,15 +1016,15 @@ RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uin
       const uint32_t c = __reduce_add_sync(RB_FULL, h0m);
       if (lane == 0 && c) atomicAdd(s_p1, c);
     }
-    // Longer rows that did not hit: the (lane, k) pairs are compacted across
-    // the warp through shared memory so every lane continues one row (up to
-    // kK2 checks, 4 per step); rows longer still are finished by the whole warp.
     uint32_t* fm_s = s_found;  // KB words: found bits per word
 #pragma unroll
     for (int k = 0; k < KB; ++k) {
       const uint32_t fm = __ballot_sync(RB_FULL, (foundm >> k) & 1u);
       if (lane == 0) fm_s[k] = fm;
     }
+    // Longer rows that did not hit: the (lane, k) pairs are compacted across
+    // the warp through shared memory so every lane continues one row (up to
+    // kK2 checks, 4 per step); rows longer still are finished by the whole warp.
     const uint32_t np = __popc(needm);
     const uint32_t incl = rb::warp_incl_scan(np);
     const uint32_t npairs = __shfl_sync(RB_FULL, incl, 31);
@@ -1024,7 +1034,7 @@ RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uin
         uint32_t pos = npend + incl - np;
         for (uint32_t m = needm; m; m &= m - 1) {
           const uint32_t k = __ffs(m) - 1;
-          s_pair[pos++] = (uint32_t)((w0 + k) * 32 + lane);
+          s_pair[pos++] = (uint32_t)(w0 * 32 + step_off(lane, k));
         }
         npend += npairs;
       }
@@ -1059,7 +1069,7 @@ RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uin
       uint32_t pos = incl - np;
       for (uint32_t m = needm; m; m &= m - 1) {
         const uint32_t k = __ffs(m) - 1;
-        s_pair[pos] = (min(dg[k], 0xffffffu) << 8) | (k << 5) | lane;  // degree saturates at 2^24-1
+        s_pair[pos] = (min(dg[k], 0xffffffu) << 8) | step_off(lane, k);  // degree saturates at 2^24-1
         ++pos;
       }
       __syncwarp();

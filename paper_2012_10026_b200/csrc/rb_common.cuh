@@ -75,6 +75,20 @@ __device__ __forceinline__ void grid_barrier_fetch(uint32_t* bar, uint32_t nbloc
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
+// *p |= v (fire-and-forget) if c, predicated.
+__device__ __forceinline__ void red_or_if(uint32_t* p, uint32_t v, bool c) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.relaxed.gpu.global.or.b32 [%0], %1;\n\t}" ::"l"(p),
+               "r"(v), "r"((uint32_t)c)
+               : "memory");
+}
+
+// *p = v if c, as one predicated store (no branch around it).
+__device__ __forceinline__ void st_if(int32_t* p, int32_t v, bool c) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.global.b32 [%0], %1;\n\t}" ::"l"(p), "r"(v),
+               "r"((uint32_t)c)
+               : "memory");
+}
+
 // Warp inclusive scan (32-bit).
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
   const uint32_t lane = lane_id();
