@@ -749,6 +749,25 @@ RB_LEVEL_FN void td_hubs(const TdCtx& c, const QEnt* hq, const uint32_t* hs, uin
 // ---------------------------------------------------------------------------
 // bottom-up
 
+// First frontier neighbour among 8 probed ones (absent: u = -1 with b = 0, a
+// prefix-valid chunk): sets par to it and returns the checks the scan order
+// spends on the chunk -- up to the hit, else every valid entry.  Branch-free
+// (a mask, predicated moves) instead of a dependent per-entry chain.
+__device__ __forceinline__ uint32_t chunk_first_hit(const int32_t (&u)[8], const uint32_t (&b)[8], int32_t& par) {
+  uint32_t hm = 0, nv = 0;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    hm |= ((b[t] >> (u[t] & 31)) & 1u) << t;
+    nv += u[t] >= 0 ? 1u : 0u;
+  }
+  int32_t first = -1;
+#pragma unroll
+  for (int t = 7; t >= 0; --t)
+    if ((hm >> t) & 1u) first = u[t];
+  if (hm) par = first;
+  return hm ? (uint32_t)__ffs(hm) : nv;
+}
+
 template <bool kRev>
 __device__ __forceinline__ int64_t bu_idx(int64_t s, int64_t e, int64_t k) {
   return kRev ? e - 1 - k : s + k;
@@ -848,13 +867,7 @@ RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uin
           uu[t] = (t0 + t < lim) ? rb::ldg_i32(p.col_bu + bu_idx<kRev>(s0, e0, t0 + t)) : -1;
 #pragma unroll
         for (int t = 0; t < 8; ++t) bb[t] = uu[t] >= 0 ? ld_bits(fcur + (uu[t] >> 5)) : 0u;
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          if (par < 0 && uu[t] >= 0) {
-            ++chk;
-            if ((bb[t] >> (uu[t] & 31)) & 1u) par = uu[t];
-          }
-        }
+        chk += chunk_first_hit(uu, bb, par);
       }
     }
     uint32_t hm = __ballot_sync(RB_FULL, mine && par < 0 && d > (uint32_t)kK2);
@@ -918,17 +931,8 @@ RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uin
         xa[t] = ua[t] >= 0 ? ld_bits(fcur + (ua[t] >> 5)) : 0u;
         xb[t] = ub[t] >= 0 ? ld_bits(fcur + (ub[t] >> 5)) : 0u;
       }
-#pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        if (pa < 0 && ua[t] >= 0) {
-          ++chk;
-          if ((xa[t] >> (ua[t] & 31)) & 1u) pa = ua[t];
-        }
-        if (pb < 0 && ub[t] >= 0) {
-          ++chk;
-          if ((xb[t] >> (ub[t] & 31)) & 1u) pb = ub[t];
-        }
-      }
+      chk += chunk_first_hit(ua, xa, pa);  // (a row already found loaded no entries: 0 checks)
+      chk += chunk_first_hit(ub, xb, pb);
     }
     for (int r = 0; r < 2; ++r) {
       const int64_t s0 = r ? sb : sa;
@@ -991,16 +995,17 @@ RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uin
     uint32_t foundm = 0, needm = 0, checks = 0, dsum = 0, dmax = 0, h0m = 0;
     int32_t* const par_out = p.parent + vbase;
 #pragma unroll
-    for (int k = 0; k < KB; ++k) {  // (inactive vertices hold hv = -1: no hit)
-      const bool act = (actm >> k) & 1u;
-      const bool h0 = hv[k].x >= 0 && ((hb0[k] >> (hv[k].x & 31)) & 1u);
-      const bool h1 = !h0 && hv[k].y >= 0 && ((hb1[k] >> (hv[k].y & 31)) & 1u);
+    for (int k = 0; k < KB; ++k) {
+      // inactive vertices (and missing neighbours) hold hv = -1, hb = 0 and dg = 0,
+      // so no activity test is needed: a -1 neighbour tests bit 31 of a zero word
+      const bool h0 = (hb0[k] >> (hv[k].x & 31)) & 1u;
+      const bool h1 = !h0 && ((hb1[k] >> (hv[k].y & 31)) & 1u);
       const bool found = h0 || h1;
       h0m += h0 ? 1u : 0u;
-      checks += act ? (h0 ? 1u : min(dg[k], 2u)) : 0u;  // (a second-neighbour hit implies dg >= 2)
+      checks += h0 ? 1u : min(dg[k], 2u);  // (a second-neighbour hit implies dg >= 2)
       rb::st_if(par_out + 32 * k, h0 ? hv[k].x : hv[k].y, found);  // predicated store, no branch
       foundm |= (uint32_t)found << k;
-      needm |= (uint32_t)(act && !found && dg[k] > 2u) << k;
+      needm |= (uint32_t)(!found && dg[k] > 2u) << k;
       dsum += found ? dg[k] : 0u;
       dmax = max(dmax, found ? dg[k] : 0u);
     }
@@ -1095,13 +1100,7 @@ RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uin
               uu[t] = (t0 + t < lim) ? rb::ldg_i32(p.col_bu + bu_idx<kRev>(s0, e0, t0 + t)) : -1;
 #pragma unroll
             for (int t = 0; t < 8; ++t) bb[t] = uu[t] >= 0 ? ld_bits(fcur + (uu[t] >> 5)) : 0u;
-#pragma unroll
-            for (int t = 0; t < 8; ++t) {
-              if (par < 0 && uu[t] >= 0) {
-                ++checks;
-                if ((bb[t] >> (uu[t] & 31)) & 1u) par = uu[t];
-              }
-            }
+            checks += chunk_first_hit(uu, bb, par);
           }
         }
         uint32_t hm = __ballot_sync(RB_FULL, mine && par < 0 && d > (uint32_t)kK2);
@@ -1216,12 +1215,7 @@ __device__ void bu_sparse_pass(const KParams& p, int64_t L, const uint32_t* fcur
                 uu[k] = (t0 + k < lim) ? rb::ldg_i32(p.col_bu + bu_idx<kRev>(s0, e0, t0 + k)) : -1;
 #pragma unroll
               for (int k = 0; k < 8; ++k) bb[k] = uu[k] >= 0 ? ld_bits(fcur + (uu[k] >> 5)) : 0u;
-#pragma unroll
-              for (int k = 0; k < 8; ++k)
-                if (par < 0 && uu[k] >= 0) {
-                  ++checks;
-                  if ((bb[k] >> (uu[k] & 31)) & 1u) par = uu[k];
-                }
+              checks += chunk_first_hit(uu, bb, par);
             }
           }
         }
