@@ -1037,9 +1037,11 @@ RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uin
     if (!kCollect) {
       if (npairs) {  // queue the rows (global ids) behind the pending ones
         uint32_t pos = npend + incl - np;
-        for (uint32_t m = needm; m; m &= m - 1) {
-          const uint32_t k = __ffs(m) - 1;
-          s_pair[pos++] = (uint32_t)(w0 * 32 + step_off(lane, k));
+#pragma unroll
+        for (int k = 0; k < KB; ++k) {  // (unrolled, predicated: no divergent loop)
+          const bool q = (needm >> k) & 1u;
+          if (q) s_pair[pos] = (uint32_t)(w0 * 32 + step_off(lane, k));
+          pos += q ? 1u : 0u;
         }
         npend += npairs;
       }
