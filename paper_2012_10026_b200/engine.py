@@ -409,12 +409,23 @@ class _ResultPool:
         self.free: dict[int, list] = {}
         self.lock = threading.Lock()
         self.registered: set[int] = set()  # id() of mappings page-locked with cudaHostRegister
+        self.seen: set[int] = set()  # sizes requested so far
 
     def get(self, nbytes: int, register: bool = False):
         with self.lock:
             lst = self.free.get(nbytes)
             if lst:
                 return lst.pop()
+            first = nbytes not in self.seen
+            self.seen.add(nbytes)
+        if first and self.keep > 1:
+            # a caller that keeps the previous result while asking for the next
+            # (res = eng.run(...) in a loop) needs two: make the spare now, not
+            # in the middle of the loop (a fresh mapping + page lock costs ~40 ms)
+            self.put(self._new(nbytes, register))
+        return self._new(nbytes, register)
+
+    def _new(self, nbytes: int, register: bool):
         m = mmap.mmap(-1, nbytes, flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
         if hasattr(m, "madvise") and hasattr(mmap, "MADV_HUGEPAGE"):
             m.madvise(mmap.MADV_HUGEPAGE)
