@@ -63,6 +63,9 @@ def parse():
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: shard the 64 independent roots over per-GPU graph replicas (throughput mode). "
                          "Default: ONE traversal per root over the 1D vertex-block partition of all GPUs")
+    ap.add_argument("--dump-levels", default=None,
+                    help="write every timed root's level records (direction, executed, n_f, m_f, scanned, byte-model "
+                         "bytes, device seconds) to this JSON file: the data roofline.by_direction is computed from")
     ap.add_argument("--partitioned", action="store_true",
                     help="force the 1D-partition path (device-side exchange) also at one GPU (loopback check)")
     ap.add_argument("--validate-roots", type=int, default=N_ROOTS,
@@ -545,6 +548,18 @@ def run_ours(args):
     if world > 1:
         # roots are independent: total raw pairs of the sweep / per-GPU sweep time
         line["replica_throughput_gteps"] = float(raw[got].sum()) / (sweep_ms / 1e3) / 1e9
+    if args.dump_levels:
+        dump = {"workload": workload(args)[0], "peak_gbs": peak, "n_dev": int(n_dev), "n_plus": int(n_plus_dev),
+                "byte_model": "TD: 20*n_f + 4*scanned + 8*n_next; BU: 3*n_dev/8 + 8*U + 4*scanned + 4*n_next "
+                              "(SURVEY 8(d), bench.level_bytes)",
+                "roots": [{"root": int(roots[j]), "mean_s": mean_t[j],
+                           "levels": [{"label": r.direction, "executed": r.executed_direction, "n_f": r.n_f,
+                                       "m_f": r.m_f, "scanned": r.scanned_edges, "bytes": b, "seconds": t}
+                                      for r, (_, b, t) in zip(levels_of[j], level_bytes(levels_of[j], n_dev,
+                                                                                          n_plus_dev))]}
+                          for j in my]}
+        with open(args.dump_levels, "w") as f:
+            json.dump(dump, f)
     if not args.no_cpu_baseline and not args.profile_roots and world == 1:
         try:
             line["cpu_baseline"] = cpu_baseline_sample(g2, roots, raw, args.cpu_seconds)
