@@ -821,7 +821,7 @@ __device__ __forceinline__ uint32_t step_off_t(uint32_t lane, uint32_t k) {
   return (k << 5) | lane;
 }
 
-template <bool kRev, int KB, bool kCollect>
+template <bool kRev, int KB, bool kCollect, bool kP1 = false>
 RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uint32_t* fnext, uint8_t* nznext,
                          Acc& acc, uint32_t* s_found, uint32_t* s_pair, uint32_t* s_next, uint32_t* ulist,
                          unsigned long long* ulist_count, uint32_t* s_p1) {
@@ -1001,7 +1001,7 @@ RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uin
       const bool h0 = (hb0[k] >> (hv[k].x & 31)) & 1u;
       const bool h1 = !h0 && ((hb1[k] >> (hv[k].y & 31)) & 1u);
       const bool found = h0 || h1;
-      h0m += h0 ? 1u : 0u;
+      if (kP1) h0m += h0 ? 1u : 0u;
       checks += h0 ? 1u : min(dg[k], 2u);  // (a second-neighbour hit implies dg >= 2)
       rb::st_if(par_out + 32 * k, h0 ? hv[k].x : hv[k].y, found);  // predicated store, no branch
       foundm |= (uint32_t)found << k;
@@ -1017,15 +1017,17 @@ RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uin
     acc.n += __popc(foundm);
     acc.deg += dsum;
     acc.maxdeg = max(acc.maxdeg, dmax);
-    if (s_p1) {  // partitioned modes: first-neighbour hits (bu_reduced pass 1)
+    if (kP1 && s_p1) {  // partitioned modes: first-neighbour hits (bu_reduced pass 1)
       const uint32_t c = __reduce_add_sync(RB_FULL, h0m);
       if (lane == 0 && c) atomicAdd(s_p1, c);
     }
-    uint32_t* fm_s = s_found;  // KB words: found bits per word
+    uint32_t* fm_s = s_found;  // KB words: found bits per word (the non-deferred path)
+    uint32_t my_fm = 0;         // lane k < KB: the found bits of word k
 #pragma unroll
     for (int k = 0; k < KB; ++k) {
       const uint32_t fm = __ballot_sync(RB_FULL, (foundm >> k) & 1u);
-      if (lane == 0) fm_s[k] = fm;
+      if (lane == (uint32_t)k) my_fm = fm;
+      if ((kCollect || !RB_BU_DEFER_CONT) && lane == 0) fm_s[k] = fm;
     }
     // Longer rows that did not hit: the (lane, k) pairs are compacted across
     // the warp through shared memory so every lane continues one row (up to
@@ -1046,13 +1048,10 @@ RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uin
         npend += npairs;
       }
       __syncwarp();
-      if (lane < (uint32_t)KB) {  // round-1 results: the warp owns these words
-        const uint32_t fm = fm_s[lane];
-        if (fm) {
-          fnext[w0 + lane] = fm;
-          nznext[w0 + lane] = 1u;
-          p.vis[w0 + lane] = vw | fm;
-        }
+      if (lane < (uint32_t)KB && my_fm) {  // round-1 results: the warp owns these words
+        fnext[w0 + lane] = my_fm;
+        nznext[w0 + lane] = 1u;
+        p.vis[w0 + lane] = vw | my_fm;
       }
       __syncwarp();
       if constexpr (KB == 8) {
@@ -1759,8 +1758,8 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
         bu_level<kRev, KB, true>(p, L, fcur, fnext, nz_of(p, r1), acc, s_bu_found[wib], s_bu_pair[wib],
                                  &s_bu_next[L & 1], lout, &out->ul_count, nullptr);
       } else
-        bu_level<kRev, KB, false>(p, L, fcur, fnext, nz_of(p, r1), acc, s_bu_found[wib], s_bu_pair[wib],
-                                  &s_bu_next[L & 1], nullptr, nullptr, (kPart && p.count_p1) ? &s_p1 : nullptr);
+        bu_level<kRev, KB, false, kPart>(p, L, fcur, fnext, nz_of(p, r1), acc, s_bu_found[wib], s_bu_pair[wib],
+                                         &s_bu_next[L & 1], nullptr, nullptr, (kPart && p.count_p1) ? &s_p1 : nullptr);
     }
     if (p.dbg && (threadIdx.x & 31) == 0 && done < 64)  // RB_DEBUG_TS: per-warp end of work
       p.dbg[kDbgWarpBase + ((uint64_t)done * gridDim.x + blockIdx.x) * kWarps + (threadIdx.x >> 5)] = globaltimer();
