@@ -531,6 +531,7 @@ def run_ours(args):
         "depth_median": float(np.median([len(levels_of[j]) for j in my])) - 1,
         "preprocessing_s": prep,
         "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                     "frac_of_nominal_8tbs": ach / 8000.0,  # the north star's nominal HBM3e figure
                      "peak_kind": peak_kind, "kernel": "bfs_persistent",
                      "bytes_per_launch": float(np.mean(bytes_alg)),
                      "launch_ms": 1e3 * float(np.mean([mean_t[j] for j in my])),

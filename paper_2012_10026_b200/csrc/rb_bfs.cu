@@ -113,6 +113,8 @@ constexpr int kK2 = 258;                         // bottom-up: per-lane checks b
 constexpr int kHeavyPerLane = 8;                 // warp-cooperative bottom-up: neighbours per lane per step
 constexpr uint64_t kDbgWarpBase = 65536;  // RB_DEBUG_TS buffer: per-block stamps, then per-warp stamps
 constexpr uint64_t kDbgPhase = 60000;     // RB_DEBUG_TS: CTA 0 phase stamps, 8 per level (top-down sub-phases)
+constexpr uint64_t kDbgWarpA = kDbgWarpBase + 64ull * 256 * 32;  // RB_DEBUG_TS: per-warp end of top-down phase A
+constexpr uint64_t kDbgWarpB = kDbgWarpA + 64ull * 256 * 32;     // RB_DEBUG_TS: per-warp end of top-down phase B
 constexpr int64_t kRecCap = 4096;                // level records per launch
 
 // Queue entry: a light frontier row (d <= kLightDeg) or one hub slice
@@ -160,6 +162,7 @@ struct KParams {
   const int32_t* col_bu;
   const int32_t* deg;
   const int2* hot;  // per vertex: the first two neighbours in bottom-up scan order (-1 = none)
+  const uint8_t* deg8;  // min(degree, 255) per vertex, zero-padded to n_words * 32 (count_next)
   int64_t n_dev;
   int64_t n_words;  // multiple of 32 * kUB
   uint32_t* vis;
@@ -526,7 +529,7 @@ __device__ __forceinline__ void td_list(const TdCtx& c, const uint32_t* lst, uin
 // batch ahead, its words in flight).  The nonzero words of a batch are
 // compacted into the warp's shared-memory list, at most 256 rows per round
 // (popc + warp scan + a loop over each lane's set bits).
-RB_LEVEL_FN void td_rows_words(const TdCtx& c, QEnt* hq, uint32_t* hs, unsigned long long* hq_count, Acc& acc,
+RB_LEVEL_FN void td_rows_words_small(const TdCtx& c, QEnt* hq, uint32_t* hs, unsigned long long* hq_count, Acc& acc,
                                uint32_t* lst,
                               uint32_t* s_next) {
   const KParams& p = *c.p;
@@ -564,6 +567,73 @@ RB_LEVEL_FN void td_rows_words(const TdCtx& c, QEnt* hq, uint32_t* hs, unsigned 
       td_list(c, lst, tot, hq, hs, hq_count, acc);
     }
   }
+}
+
+RB_LEVEL_FN void td_rows_words_big(const TdCtx& c, QEnt* hq, uint32_t* hs, unsigned long long* hq_count, Acc& acc,
+                               uint32_t* lst,
+                              uint32_t* s_next) {
+  // A warp claims kG batches per shared-counter add and has their words in
+  // flight together; the rows of the whole group go through ONE list round when
+  // they fit (one record-load latency and one hub-row append per group instead
+  // of per batch: phase A of a 5 K-row frontier at scale 26 took 9+ dependent
+  // claim / load / append rounds per warp, 17.6 us; 13 us with groups).
+  constexpr int kG = 2;
+  static_assert(32 * kG <= kList, "a lane's rows must fit one list round");
+  const KParams& p = *c.p;
+  const uint32_t lane = rb::lane_id();
+  const uint64_t nw = (uint64_t)p.n_words_glob;
+  const uint64_t Q = (nw + 31) / 32;
+  // (groups only when every warp has several batches to do: a scale-22 bitmap is one batch per warp)
+  const uint32_t g = Q >= 2ull * kG * gridDim.x * kWarps ? (uint32_t)kG : 1u;
+  while (true) {
+    uint32_t k = 0;
+    if (lane == 0) k = atomicAdd(s_next, g);
+    k = __shfl_sync(RB_FULL, k, 0);
+    if ((uint64_t)blockIdx.x + (uint64_t)k * gridDim.x >= Q) break;
+    uint32_t x[kG], vb[kG];
+    uint32_t cnt;
+#pragma unroll
+    for (int j = 0; j < kG; ++j) {
+      const uint64_t q = (uint64_t)blockIdx.x + (uint64_t)(k + j) * gridDim.x;
+      const uint64_t w = q + (uint64_t)lane * Q;
+      x[j] = ((uint32_t)j < g && q < Q && w < nw) ? __ldcg(c.fcur + w) : 0u;
+      vb[j] = (uint32_t)(w * 32);
+    }
+    while (true) {
+      // the rows of a prefix of the lanes that fits the 256-entry list (a lane
+      // holds at most 32 kG <= kList rows, so every round makes progress)
+      cnt = 0;
+#pragma unroll
+      for (int j = 0; j < kG; ++j) cnt += __popc(x[j]);
+      const uint32_t incl = rb::warp_incl_scan(cnt);
+      const bool take = incl <= (uint32_t)kList;
+      const uint32_t tot = __reduce_max_sync(RB_FULL, take ? incl : 0u);
+      if (tot == 0) break;
+      __syncwarp();
+      if (take) {
+        uint32_t pos = incl - cnt;
+#pragma unroll
+        for (int j = 0; j < kG; ++j) {
+          for (uint32_t y = x[j]; y; y &= y - 1) lst[pos++] = vb[j] + (__ffs(y) - 1);
+          x[j] = 0u;
+        }
+      }
+      __syncwarp();
+      td_list(c, lst, tot, hq, hs, hq_count, acc);
+    }
+  }
+}
+
+// Small graphs (4-word bottom-up build) keep the one-batch-ahead loop: their
+// bitmap is about one batch per warp, and the grouped loop measured 2 % slower
+// at scale 22.
+template <bool kBig>
+__device__ __forceinline__ void td_rows_words(const TdCtx& c, QEnt* hq, uint32_t* hs, unsigned long long* hq_count,
+                                              Acc& acc, uint32_t* lst, uint32_t* s_next) {
+  if constexpr (kBig)
+    td_rows_words_big(c, hq, hs, hq_count, acc, lst, s_next);
+  else
+    td_rows_words_small(c, hq, hs, hq_count, acc, lst, s_next);
 }
 
 // Top-down phase A from a frontier list (the one the solo levels leave):
@@ -627,7 +697,100 @@ RB_LEVEL_FN void td_rows_items(const TdCtx& c, const uint8_t* nzcur, QEnt* hq, u
 // level start) becomes the next frontier vis & ~fnext, with its nonzero
 // summary; counters n_next = popcount, deg_next = sum of the degrees of the
 // new bits, max degree.  Streaming passes instead of per-claim random traffic.
-__device__ void count_next(const KParams& p, uint32_t* fnext, uint8_t* nznext, Acc& acc) {
+struct CnArgs {  // the fields count_next reads
+  const uint32_t* vis;
+  const uint8_t* deg8;
+  const int32_t* deg;
+  uint64_t n_words;
+  int64_t n_dev;
+};
+__device__ __forceinline__ Acc count_next_fn(const CnArgs p, uint32_t* fnext, uint8_t* nznext) {
+  Acc acc{0, 0, 0, 0u};
+  // Lane l owns word w0 + l: its next-frontier bits, and -- if any -- the 32
+  // degrees of that word from the saturating 8-bit copy deg8 (ONE sector per
+  // word, two 16-B loads; the int32 degrees cost four sectors and made this
+  // pass read the whole 4 n_dev-byte array on every deferred level).  Bits are
+  // spread to byte masks by a carry-free multiply, selected bytes summed with
+  // dp4a; a selected byte of 255 (degree >= 255: the high-id hub region only)
+  // reads the exact degree.
+  // kCN words per lane per round, every load of a round in flight together
+  // (the pass is a chain of dependent round trips per warp, not bandwidth).
+  constexpr int kCN = 4;
+  const uint32_t lane = rb::lane_id();
+  const uint64_t nw = (uint64_t)p.n_words;
+  const uint64_t stride = (uint64_t)gridDim.x * kWarps * 32;
+  for (uint64_t w0 = warp_slot() * 32; w0 < nw; w0 += kCN * stride) {
+    uint32_t x[kCN];
+#pragma unroll
+    for (int r = 0; r < kCN; ++r) {
+      const uint64_t w = w0 + r * stride + lane;
+      x[r] = w < nw ? (__ldcg(p.vis + w) & ~__ldcg(fnext + w)) : 0u;
+    }
+    uint4 qa[kCN], qb[kCN];
+#pragma unroll
+    for (int r = 0; r < kCN; ++r) {
+      const uint64_t w = w0 + r * stride + lane;
+      qa[r] = qb[r] = make_uint4(0u, 0u, 0u, 0u);
+      if (x[r]) {  // (deg8 is padded to n_words * 32)
+        const uint4* dp = reinterpret_cast<const uint4*>(p.deg8 + (int64_t)w * 32);
+        qa[r] = __ldg(dp);
+        qb[r] = __ldg(dp + 1);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kCN; ++r) {
+      const uint64_t w = w0 + r * stride + lane;
+      if (w < nw) {
+        fnext[w] = x[r];
+        nznext[w] = x[r] != 0u ? 1u : 0u;
+      }
+      acc.n += __popc(x[r]);
+      const uint32_t q[8] = {qa[r].x, qa[r].y, qa[r].z, qa[r].w, qb[r].x, qb[r].y, qb[r].z, qb[r].w};
+      uint32_t sum = 0, mx = 0, sat = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        // bits 4j .. 4j+3 of x -> 0xFF in bytes 0 .. 3 (bit k lands on bit 8k: k + 7k, no carries)
+        const uint32_t m = ((((x[r] >> (4 * j)) & 0xFu) * 0x00204081u) & 0x01010101u) * 0xFFu;
+        const uint32_t sel = q[j] & m;
+        sum = __dp4a(sel, 0x01010101u, sum);
+        mx = __vmaxu4(mx, sel);
+        sat |= __vcmpeq4(sel, 0xFFFFFFFFu);
+      }
+      uint32_t dmax = max(max(mx & 0xFFu, (mx >> 8) & 0xFFu), max((mx >> 16) & 0xFFu, mx >> 24));
+      if (sat) {  // a selected degree >= 255 (hub region): the word's exact degrees, all loads in flight
+        sum = 0;
+        dmax = 0;
+        if ((int64_t)(w + 1) * 32 <= p.n_dev) {
+          const int4* dq = reinterpret_cast<const int4*>(p.deg + (int64_t)w * 32);
+          int4 f[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) f[j] = __ldg(dq + j);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t dv[4] = {(uint32_t)f[j].x, (uint32_t)f[j].y, (uint32_t)f[j].z, (uint32_t)f[j].w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const uint32_t d = ((x[r] >> (4 * j + t)) & 1u) ? dv[t] : 0u;
+              sum += d;
+              dmax = max(dmax, d);
+            }
+          }
+        } else {  // the word holding the end of the vertex range: no reads past deg[n_dev)
+          for (uint32_t y = x[r]; y; y &= y - 1) {
+            const uint32_t d = (uint32_t)rb::ldg_i32(p.deg + (int64_t)w * 32 + (__ffs(y) - 1));
+            sum += d;
+            dmax = max(dmax, d);
+          }
+        }
+      }
+      acc.deg += sum;
+      acc.maxdeg = max(acc.maxdeg, dmax);
+    }
+  }
+  return acc;
+}
+
+__device__ __forceinline__ void count_next_small(const KParams& p, uint32_t* fnext, uint8_t* nznext, Acc& acc) {
   // Lane l owns word w0 + l: its next-frontier bits, and -- if any -- the 32
   // degrees of that word as eight 16-B loads, all in flight together (one
   // round trip per 32 words instead of one per 4 nonzero words).
@@ -663,6 +826,19 @@ __device__ void count_next(const KParams& p, uint32_t* fnext, uint8_t* nznext, A
         acc.maxdeg = max(acc.maxdeg, d);
       }
     }
+  }
+}
+
+template <bool kBig>
+__device__ __forceinline__ void count_next(const KParams& p, uint32_t* fnext, uint8_t* nznext, Acc& acc) {
+  if constexpr (kBig) {
+    const CnArgs a{p.vis, p.deg8, p.deg, (uint64_t)p.n_words, p.n_dev};
+    const Acc r = count_next_fn(a, fnext, nznext);
+    acc.n += r.n;
+    acc.deg += r.deg;
+    acc.maxdeg = max(acc.maxdeg, r.maxdeg);
+  } else {
+    count_next_small(p, fnext, nznext, acc);  // (one round per warp at scale 22: the exact degrees in one round trip)
   }
 }
 
@@ -957,34 +1133,42 @@ RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uin
     if (pb >= 0) found_one(vb, pb, db);
   };
 #endif
+  auto load_vis = [&](uint64_t w) -> uint32_t {
+    return (w < nw && lane < KB) ? __ldcg(p.vis + w + lane) : 0xffffffffu;
+  };
+  // lane l owns vertex (w + k) * 32 + l of each of the step's KB words: bit k = that vertex is unvisited
+  auto act_of = [&](uint32_t vwx) -> uint32_t {
+    uint32_t m = 0;
+#pragma unroll
+    for (int k = 0; k < KB; ++k) m |= ((~__shfl_sync(RB_FULL, vwx, k) >> lane) & 1u) << k;
+    return m;
+  };
+  // round-1 records of a step: the two scan-first neighbours and the degree, coalesced, all loads in flight
+  auto load_rec = [&](uint64_t w, uint32_t m, int2 (&hvx)[KB], uint32_t (&dgx)[KB]) {
+    const int64_t vb = (int64_t)w * 32 + lane;
+#pragma unroll
+    for (int k = 0; k < KB; ++k) {
+      hvx[k] = make_int2(-1, -1);
+      dgx[k] = 0;
+      if ((m >> k) & 1u) {
+        hvx[k] = __ldg(p.hot + vb + 32 * k);
+        dgx[k] = (uint32_t)rb::ldg_i32(p.deg + vb + 32 * k);
+      }
+    }
+  };
   uint64_t w_nx = claim_step();
-  uint32_t vw_nx = (w_nx < nw && lane < KB) ? __ldcg(p.vis + w_nx + lane) : 0xffffffffu;
+  uint32_t vw_nx = load_vis(w_nx);
   while (w_nx < nw) {
     const uint64_t w0 = w_nx;
     const uint32_t vw = vw_nx;
     w_nx = claim_step();
-    vw_nx = (w_nx < nw && lane < KB) ? __ldcg(p.vis + w_nx + lane) : 0xffffffffu;
-    // lane l owns vertex (w0 + k) * 32 + l of each of the KB words
-    uint32_t actm = 0;
-#pragma unroll
-    for (int k = 0; k < KB; ++k) actm |= ((~__shfl_sync(RB_FULL, vw, k) >> lane) & 1u) << k;
+    vw_nx = load_vis(w_nx);
+    const uint32_t actm = act_of(vw);
     if (!__any_sync(RB_FULL, actm != 0)) continue;
-    const int64_t vbase = (int64_t)w0 * 32 + lane;
-    const int32_t* const deg = p.deg + vbase;
-    // round 1: the two scan-first neighbours (and the degree) from the
-    // compact side record, coalesced -- all KB loads in flight
     int2 hv[KB];
     uint32_t dg[KB];
-    const int2* const hot = p.hot + vbase;
-#pragma unroll
-    for (int k = 0; k < KB; ++k) {
-      hv[k] = make_int2(-1, -1);
-      dg[k] = 0;
-      if ((actm >> k) & 1u) {
-        hv[k] = __ldg(hot + 32 * k);
-        dg[k] = (uint32_t)__ldg(deg + 32 * k);
-      }
-    }
+    load_rec(w0, actm, hv, dg);
+    const int64_t vbase = (int64_t)w0 * 32 + lane;
     uint32_t hb0[KB], hb1[KB];
 #pragma unroll
     for (int k = 0; k < KB; ++k) {
@@ -1726,10 +1910,12 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
       if (s_fin[8] && done == (int64_t)s_fin[0])  // the first grid level after the solo levels
         td_rows_list(c, p.solo_q, (uint32_t)s_fin[8], hq, hs, &in->hq_count, acc, s_bu_pair[threadIdx.x >> 5]);
       else if (nf >= kDenseFrontier)
-        td_rows_words(c, hq, hs, &in->hq_count, acc, s_bu_pair[threadIdx.x >> 5], &s_bu_next[L & 1]);
+        td_rows_words<KB == 8>(c, hq, hs, &in->hq_count, acc, s_bu_pair[threadIdx.x >> 5], &s_bu_next[L & 1]);
       else
         td_rows_items(c, p.nzcur_ext ? p.nzcur_ext : nz_of(p, r0), hq, hs, &in->hq_count, acc,
                       s_bu_pair[threadIdx.x >> 5]);
+      if (p.dbg && (threadIdx.x & 31) == 0 && done < 64)
+        p.dbg[kDbgWarpA + ((uint64_t)done * gridDim.x + blockIdx.x) * kWarps + (threadIdx.x >> 5)] = globaltimer();
       if (hubs) {  // phase B only if some frontier row has more than kLightDeg edges
         {
           const unsigned long long* const src[1] = {&in->hq_count};
@@ -1738,12 +1924,14 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
         if (blockIdx.x == 0 && threadIdx.x == 32) t_queue = globaltimer() - t_prev;
         if (p.dbg && blockIdx.x == 0 && threadIdx.x == 0 && done < 64) p.dbg[kDbgPhase + done * 8 + 1] = globaltimer();
         td_hubs(c, hq, hs, s_ctr[0] >> 40, s_ctr[0] & kSliceMask, acc);
+        if (p.dbg && (threadIdx.x & 31) == 0 && done < 64)
+          p.dbg[kDbgWarpB + ((uint64_t)done * gridDim.x + blockIdx.x) * kWarps + (threadIdx.x >> 5)] = globaltimer();
       }
       if (p.dbg && blockIdx.x == 0 && threadIdx.x == 0 && done < 64) p.dbg[kDbgPhase + done * 8 + 2] = globaltimer();
       if (c.defer) {
         rb::grid_barrier(p.bar, nblocks, epoch);  // every claim of the level has landed
         if (p.dbg && blockIdx.x == 0 && threadIdx.x == 0 && done < 64) p.dbg[kDbgPhase + done * 8 + 3] = globaltimer();
-        count_next(p, fnext, nz_of(p, r1), acc);
+        count_next<KB == 8>(p, fnext, nz_of(p, r1), acc);
         if (p.dbg && blockIdx.x == 0 && threadIdx.x == 0 && done < 64) p.dbg[kDbgPhase + done * 8 + 4] = globaltimer();
       }
     } else {
@@ -1910,6 +2098,14 @@ __global__ void make_hot(const int64_t* rs, const int32_t* col, int64_t n, int r
   }
 }
 
+// deg8[v] = min(deg[v], 255) for v < n, 0 up to n_pad
+__global__ void make_deg8(const int32_t* deg, int64_t n, int64_t n_pad, uint8_t* deg8) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n_pad; v += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t d = v < n ? deg[v] : 0;
+    deg8[v] = (uint8_t)(d < 255 ? d : 255);
+  }
+}
+
 // *out += number of zero bits of words[0, n) (unvisited-at-start vertices)
 __global__ void count_zero_bits(const uint32_t* words, int64_t n, unsigned long long* out) {
   unsigned long long c = 0;
@@ -2064,7 +2260,7 @@ __device__ void dist_body(const KParams& p, const XParams& x, int64_t L, int xdi
       rb::grid_barrier(p.bar, nblocks, epoch);
     }
     if (nf >= kDenseFrontier)
-      td_rows_words(c, hq, hs, &in->hq_count, acc, sm.bu_pair[threadIdx.x >> 5], &sm.next_step);
+      td_rows_words<KB == 8>(c, hq, hs, &in->hq_count, acc, sm.bu_pair[threadIdx.x >> 5], &sm.next_step);
     else
       td_rows_items(c, x.xnz[r0], hq, hs, &in->hq_count, acc, sm.bu_pair[threadIdx.x >> 5]);
     if (hubs) {
@@ -2074,7 +2270,7 @@ __device__ void dist_body(const KParams& p, const XParams& x, int64_t L, int xdi
     }
     if (c.defer) {
       rb::grid_barrier(p.bar, nblocks, epoch);
-      count_next(p, fnext, nz_of(p, r1), acc);
+      count_next<KB == 8>(p, fnext, nz_of(p, r1), acc);
     }
   } else {
     const uint32_t wib = threadIdx.x >> 5;
@@ -2303,6 +2499,7 @@ struct rb_bfs {
   uint32_t* vis_template;   // isolated + padding premarked
   uint32_t* pad_mask;       // padding bits only
   int2* hot;
+  uint8_t* deg8;
   VInfo* vinfo;
   VInfo* td_vinfo;  // partitioned engines only
   int64_t n_glob;
@@ -2448,6 +2645,7 @@ extern "C" int rb_bfs_create_part(const int64_t* d_row_starts, const int32_t* d_
 
   RB_ALLOC(k.parent, (size_t)n_dev * 4);
   RB_ALLOC(h->hot, (size_t)n_dev * sizeof(int2));
+  RB_ALLOC(h->deg8, (size_t)h->n_words * 32);
   if (params->record_levels) RB_ALLOC(k.level, (size_t)n_dev * 4);
   RB_ALLOC(k.slots, 3 * sizeof(Slot));
   RB_ALLOC(k.bar, 64);
@@ -2467,6 +2665,8 @@ extern "C" int rb_bfs_create_part(const int64_t* d_row_starts, const int32_t* d_
   make_pad_mask<<<256, 256>>>(h->pad_mask, n_dev, h->n_words);
   make_hot<<<1024, 256>>>(d_row_starts, k.col_bu, n_dev, params->bu_reverse, h->hot);
   k.hot = h->hot;
+  make_deg8<<<1024, 256>>>(d_degrees, n_dev, h->n_words * 32, h->deg8);
+  k.deg8 = h->deg8;
   make_vinfo<<<1024, 256>>>(d_row_starts, d_col, n_dev, h->vinfo);
   k.vinfo = h->vinfo;
   k.hubs0 = -1;
@@ -2536,7 +2736,7 @@ extern "C" int rb_bfs_destroy(rb_bfs* h) {
   if (!h) return RB_OK;
   KParams& k = h->kp;
   void* ptrs[] = {k.vis, k.fb0, k.fb1, k.fb2, h->vis_template, h->pad_mask, k.hq0, k.hq1, k.hs0, k.hs1, k.ul0, k.ul1, k.solo_q, k.parent,
-                  k.level, k.slots, k.bar, k.rec, k.fin, k.nz0, k.nz1, k.nz2, h->hot, h->vinfo, k.dbg, h->td_vinfo,
+                  k.level, k.slots, k.bar, k.rec, k.fin, k.nz0, k.nz1, k.nz2, h->hot, h->deg8, h->vinfo, k.dbg, h->td_vinfo,
                   h->part_dev};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -2839,7 +3039,7 @@ extern "C" int rb_bfs_barrier_probe(rb_bfs* h, int iters, double* ns_per_barrier
 
 extern "C" int rb_bfs_debug_timestamps(rb_bfs* h, uint64_t* out, int64_t cap, int* blocks) {
   if (!h || !h->kp.dbg) return rb_null_handle(__func__);
-  const int64_t n = (int64_t)kDbgWarpBase + (int64_t)64 * h->blocks * kWarps;  // see kDbgWarpBase
+  const int64_t n = (int64_t)kDbgWarpBase + (int64_t)64 * 1024 * kWarps;  // the whole buffer (see kDbgWarpBase / A / B)
   RB_CUDA_TRY(cudaMemcpy(out, h->kp.dbg, (size_t)(n < cap ? n : cap) * 8, cudaMemcpyDeviceToHost));
   *blocks = h->blocks;
   return RB_OK;
