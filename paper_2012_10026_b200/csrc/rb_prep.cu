@@ -28,6 +28,7 @@
 #include <cub/cub.cuh>
 #include <stdint.h>
 #include <stdio.h>
+#include <string.h>
 
 #include <algorithm>
 #include <vector>
@@ -438,6 +439,41 @@ __global__ void gather_rows(const int64_t* __restrict__ rs, const int32_t* __res
   }
 }
 
+// Relabel by transposition (undirected graphs: every edge is stored in both
+// directions).  New row nv = old row perm[nv]; its entries are emitted as pairs
+// (key = the neighbour's new id, value = nv) in new-row order.  A STABLE sort by
+// key then lists, for every new vertex x, the new ids of the vertices adjacent
+// to it in ascending order -- by symmetry exactly row x of the relabelled graph
+// -- so the sorted values ARE the new column array: log2(n) key bits of one
+// radix sort instead of a sort inside every row (the segmented sort of the hub
+// rows was the largest preprocessing cost at scale 26).
+__global__ void relabel_pairs(const int64_t* __restrict__ rs, const int32_t* __restrict__ col,
+                              const uint32_t* __restrict__ perm, const uint32_t* __restrict__ inv,
+                              const int64_t* __restrict__ rs_new, int64_t n, uint32_t* __restrict__ keys,
+                              uint32_t* __restrict__ vals) {
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int64_t nv = warp; nv < n; nv += nwarps) {
+    const uint32_t ov = perm[nv];
+    const int64_t s = rs[ov], e = rs[ov + 1], b = rs_new[nv];
+    for (int64_t j = s + lane; j < e; j += 32) {
+      keys[b + (j - s)] = inv[col[j]];
+      vals[b + (j - s)] = (uint32_t)nv;
+    }
+  }
+}
+
+// The sorted keys must fill every new row exactly (key x on [rs_new[x], rs_new[x+1])):
+// true for a symmetric graph; *bad counts the rows where it fails.
+__global__ void relabel_check(const uint32_t* __restrict__ keys, const int64_t* __restrict__ rs_new, int64_t n,
+                              unsigned long long* __restrict__ bad) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = rs_new[v], e = rs_new[v + 1];
+    if (e > s && (keys[s] != (uint32_t)v || keys[e - 1] != (uint32_t)v)) atomicAdd(bad, 1ull);
+  }
+}
+
 __global__ void degree_keys(const int64_t* __restrict__ rs, const int32_t* __restrict__ col,
                             const int32_t* __restrict__ deg, int64_t n, int descending, uint64_t* __restrict__ keys) {
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -807,6 +843,15 @@ extern "C" int rb_rcm(const int64_t* d_rs, const int32_t* d_col, const int32_t* 
 
 // ---------------------------------------------------------------------------
 
+namespace {
+size_t pair_sort_temp_bytes(int64_t m) {
+  size_t t = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, t, (const uint32_t*)nullptr, (uint32_t*)nullptr, (const uint32_t*)nullptr,
+                                  (uint32_t*)nullptr, (int64_t)std::max<int64_t>(m, 1), 0, 32);
+  return t;
+}
+}  // namespace
+
 extern "C" size_t rb_permute_workspace_bytes(int64_t n, int64_t m) {
   Carver c(nullptr, SIZE_MAX);
   c.take<int64_t>((size_t)n + 1);                   // deg64 / rs scan input
@@ -815,7 +860,7 @@ extern "C" size_t rb_permute_workspace_bytes(int64_t n, int64_t m) {
   c.take<int32_t>((size_t)n + 2);                   // relative offsets
   size_t t1 = segsort_temp_bytes<int32_t>(n, m), t2 = segsort_temp_bytes<uint64_t>(n, m), t3 = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, t3, (int64_t*)nullptr, (int64_t*)nullptr, (int64_t)n + 1);
-  c.take<char>(std::max(std::max(t1, t2), t3));
+  c.take<char>(std::max(std::max(std::max(t1, t2), t3), pair_sort_temp_bytes(m)));
   return c.off + 256;
 }
 
@@ -830,12 +875,13 @@ extern "C" int rb_apply_permutation(const int64_t* d_rs, const int32_t* d_col, c
   }
   Carver c(d_ws, ws_bytes);
   int64_t* deg64 = c.take<int64_t>((size_t)n + 1);
-  int32_t* gathered = (int32_t*)c.take<uint64_t>((size_t)std::max<int64_t>(m, 1));
-  c.take<uint64_t>((size_t)std::max<int64_t>(m, 1));
+  uint64_t* area_a = c.take<uint64_t>((size_t)std::max<int64_t>(m, 1));
+  uint64_t* area_b = c.take<uint64_t>((size_t)std::max<int64_t>(m, 1));
+  int32_t* gathered = (int32_t*)area_a;
   int32_t* rel = c.take<int32_t>((size_t)n + 2);
   size_t t1 = segsort_temp_bytes<int32_t>(n, m), t2 = segsort_temp_bytes<uint64_t>(n, m), t3 = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, t3, (int64_t*)nullptr, (int64_t*)nullptr, (int64_t)n + 1);
-  const size_t tb = std::max(std::max(t1, t2), t3);
+  const size_t tb = std::max(std::max(std::max(t1, t2), t3), pair_sort_temp_bytes(m));
   void* temp = c.take<char>(tb);
   if (n == 0) {
     RB_CUDA_TRY(cudaMemsetAsync(d_rs_out, 0, 8, s));
@@ -845,6 +891,27 @@ extern "C" int rb_apply_permutation(const int64_t* d_rs, const int32_t* d_col, c
   gather_deg<<<grid_for(n), 256, 0, s>>>(d_deg, d_perm, n, d_deg_out, deg64);
   size_t t = tb;
   RB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(temp, t, deg64, d_rs_out, n + 1, s));
+  const char* mode = getenv("RB_RELABEL");  // "segsort": always sort inside the rows (tuning / A-B)
+  if (m > 0 && !(mode && strcmp(mode, "segsort") == 0)) {
+    // undirected graph: pairs (new neighbour id, new row) in new-row order, one stable radix sort by key
+    uint32_t* keys_in = reinterpret_cast<uint32_t*>(area_a);
+    uint32_t* vals_in = keys_in + m;
+    uint32_t* keys_out = reinterpret_cast<uint32_t*>(area_b);
+    unsigned long long* bad = reinterpret_cast<unsigned long long*>(deg64);  // (the scan input is free again)
+    relabel_pairs<<<grid_for(n * 32), 256, 0, s>>>(d_rs, d_col, d_perm, d_inv, d_rs_out, n, keys_in, vals_in);
+    RB_CUDA_TRY(cudaGetLastError());
+    t = tb;
+    const int bits = std::max(1, bits_for((uint64_t)(n > 0 ? n - 1 : 0)));
+    RB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(temp, t, (const uint32_t*)keys_in, keys_out, (const uint32_t*)vals_in,
+                                                reinterpret_cast<uint32_t*>(d_col_out), m, 0, bits, s));
+    RB_CUDA_TRY(cudaMemsetAsync(bad, 0, 8, s));
+    relabel_check<<<grid_for(n), 256, 0, s>>>(keys_out, d_rs_out, n, bad);
+    unsigned long long h_bad = 0;
+    RB_CUDA_TRY(cudaMemcpyAsync(&h_bad, bad, 8, cudaMemcpyDeviceToHost, s));
+    RB_CUDA_TRY(cudaStreamSynchronize(s));
+    if (h_bad == 0) return RB_OK;
+    // not symmetric (the transposed rows do not fit): fall through to the general path
+  }
   gather_rows<<<grid_for(n * 32), 256, 0, s>>>(d_rs, d_col, d_perm, d_inv, d_rs_out, n, gathered);
   RB_CUDA_TRY(cudaGetLastError());
   int rc = segmented_sort_rows<int32_t>(d_rs_out, n, m, gathered, d_col_out, temp, tb, rel, s);
