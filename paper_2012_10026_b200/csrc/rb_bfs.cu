@@ -293,6 +293,29 @@ __device__ __forceinline__ void ld_vinfo(const KParams& p, int64_t v, int64_t& s
   n1 = a.w;
 }
 
+// Deferred claim of KU edges per lane given the probed visited words.
+// Big levels: no atomic return trip and no per-winner degree load.  Every
+// frontier vertex adjacent to an unvisited w is a valid parent of w, so
+// concurrent writers of parent[w] may race -- the last store stands.  Only
+// the visited bit is set (fire-and-forget red; it also stops later probes
+// of this level): the next frontier is vis minus the copy of vis taken at
+// the level start (held in fnext), and its summary and exact counters
+// (n_next, deg_next, max degree) come from one pass over it (count_next).
+template <int KU>
+__device__ __forceinline__ void td_claim_deferred(const TdCtx& c, const int32_t (&v)[KU], const int32_t (&wl)[KU],
+                                                  const bool (&act)[KU], const uint32_t (&seen)[KU]) {
+  const KParams& p = *c.p;
+#pragma unroll
+  for (int k = 0; k < KU; ++k) {
+    const uint32_t bit = 1u << (wl[k] & 31);
+    if (act[k] && !(seen[k] & bit)) {
+      p.parent[wl[k]] = v[k];
+      if (p.level) p.level[wl[k]] = (int32_t)(c.L + 1);
+      red_or(p.vis + (wl[k] >> 5), bit);
+    }
+  }
+}
+
 // Warp-collective claim of KU edges per lane (v[k] -> w[k], act[k]).
 template <int KU>
 __device__ __forceinline__ void td_claim(const TdCtx& c, const int32_t (&v)[KU], const int32_t (&w)[KU],
@@ -303,25 +326,10 @@ __device__ __forceinline__ void td_claim(const TdCtx& c, const int32_t (&v)[KU],
 #pragma unroll
   for (int k = 0; k < KU; ++k) wl[k] = w[k] - (int32_t)p.v_lo;
   if (c.defer) {
-    // Big levels: no atomic return trip and no per-winner degree load.  Every
-    // frontier vertex adjacent to an unvisited w is a valid parent of w, so
-    // concurrent writers of parent[w] may race -- the last store stands.  Only
-    // the visited bit is set (fire-and-forget red; it also stops later probes
-    // of this level): the next frontier is vis minus the copy of vis taken at
-    // the level start (held in fnext), and its summary and exact counters
-    // (n_next, deg_next, max degree) come from one pass over it (count_next).
     uint32_t seen[KU];
 #pragma unroll
     for (int k = 0; k < KU; ++k) seen[k] = act[k] ? ld_bits(p.vis + (wl[k] >> 5)) : 0u;
-#pragma unroll
-    for (int k = 0; k < KU; ++k) {
-      const uint32_t bit = 1u << (wl[k] & 31);
-      if (act[k] && !(seen[k] & bit)) {
-        p.parent[wl[k]] = v[k];
-        if (p.level) p.level[wl[k]] = (int32_t)(c.L + 1);
-        red_or(p.vis + (wl[k] >> 5), bit);
-      }
-    }
+    td_claim_deferred<KU>(c, v, wl, act, seen);
     return;
   }
   // claim = first to set the visited bit (vis holds every discovered vertex).
@@ -577,7 +585,7 @@ RB_LEVEL_FN void td_rows_words_big(const TdCtx& c, QEnt* hq, uint32_t* hs, unsig
   // they fit (one record-load latency and one hub-row append per group instead
   // of per batch: phase A of a 5 K-row frontier at scale 26 took 9+ dependent
   // claim / load / append rounds per warp, 17.6 us; 13 us with groups).
-  constexpr int kG = 2;
+  constexpr int kG = 2;  // (4 / 8: more spills, s26 -0.4 % / -1.3 %)
   static_assert(32 * kG <= kList, "a lane's rows must fit one list round");
   const KParams& p = *c.p;
   const uint32_t lane = rb::lane_id();
@@ -843,21 +851,38 @@ __device__ __forceinline__ void count_next(const KParams& p, uint32_t* fnext, ui
 }
 
 // Top-down phase B: hub slices, one warp item each (8 edges per lane).
+#ifndef RB_TD_DYN_MINK
+#define RB_TD_DYN_MINK 16  // slices per warp from which the tail of phase B is dealt dynamically
+#endif
+#ifndef RB_TD_DYN_NUM
+#define RB_TD_DYN_NUM 3    // static share of phase B: RB_TD_DYN_NUM / 4 of the slices
+#endif
+#ifndef RB_TD_DYN_CHUNK
+#define RB_TD_DYN_CHUNK 8  // slices per dynamic claim (4: the row search per claim ate the gain)
+#endif
 RB_LEVEL_FN void td_hubs(const TdCtx& c, const QEnt* hq, const uint32_t* hs, uint64_t nrows, uint64_t nh,
-                         Acc& acc) {
+                         unsigned long long* dyn, Acc& acc) {
   // Warp g takes the contiguous slices [g*K, (g+1)*K): one row search per
   // warp, then the rows are walked in order (each warp streams its own part
   // of the column array).  Software-pipelined: the columns of the next slice
   // are in flight while the current one is probed and claimed.
+  // Big levels (dyn set, >= RB_TD_DYN_MINK slices per warp): equal slice counts
+  // do not finish together -- the warps of a scale-26 deferred level ended
+  // between 120 and 176 us (claim density and L1 hits differ by row) and the
+  // grid waited for the last one.  There only the first 3/4 of the slices are
+  // dealt statically; the rest is claimed in chunks of RB_TD_DYN_CHUNK slices
+  // from a level counter, the next claim in flight while a chunk is processed.
   const KParams& p = *c.p;
   const uint32_t lane = rb::lane_id();
   const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
-  const uint64_t K = (nh + nwarps - 1) / nwarps;
-  const uint64_t i0 = warp_slot() * K;
-  if (i0 >= nh) return;
-  uint32_t left = (uint32_t)min(K, nh - i0);  // slices still to process
-  // current slice: row entry `row` (index r), edges [row.s + o, row.s + o + 256) of it
-  int32_t w[kChunkPerLane];
+  uint64_t K = (nh + nwarps - 1) / nwarps;
+  uint64_t dyn0 = nh;  // first dynamically dealt slice
+  if (dyn && nh / nwarps >= (uint64_t)RB_TD_DYN_MINK) {
+    K = (nh / nwarps) * RB_TD_DYN_NUM / 4;
+    dyn0 = K * nwarps;
+  }
+  unsigned long long ticket = 0;
+  if (dyn0 < nh && lane == 0) ticket = atomicAdd(dyn, (unsigned long long)RB_TD_DYN_CHUNK);
   auto columns = [&](const QEnt& e, int32_t (&x)[kChunkPerLane]) {
 #pragma unroll
     for (int k = 0; k < kChunkPerLane; ++k) {
@@ -865,60 +890,73 @@ RB_LEVEL_FN void td_hubs(const TdCtx& c, const QEnt* hq, const uint32_t* hs, uin
       x[k] = j < e.d ? rb::ldg_i32(p.td_col + e.s + j) : -1;
     }
   };
-  // the row's remaining edges after the current slice, and the next row index
-  int64_t rest;   // edges of the current row after this slice
-  uint64_t rnext;  // index of the next row
-  QEnt cur;
-  {
-    uint32_t first;
-    uint64_t r0;
-    const QEnt row = row_of_slice(hq, hs, nrows, i0, &first, &r0);
-    const int64_t off = (int64_t)(i0 - first) * kChunk;
-    cur.s = row.s + off;
-    cur.v = row.v;
-    cur.d = (int32_t)min((int64_t)kChunk, (int64_t)row.d - off);
-    rest = (int64_t)row.d - off - cur.d;
-    rnext = r0 + 1;
-  }
-  columns(cur, w);
+  uint64_t i0 = warp_slot() * K;
+  uint32_t left = i0 < dyn0 ? (uint32_t)min(K, dyn0 - i0) : 0u;  // slices still to process
   while (true) {
-    // descriptor of the next slice (same row, or the start of the next row)
-    QEnt nx;
-    nx.s = 0;
-    nx.v = 0;
-    nx.d = 0;
-    int64_t nrest = 0;
-    if (left > 1) {
-      if (rest > 0) {
-        nx.s = cur.s + cur.d;
-        nx.v = cur.v;
-        nx.d = (int32_t)min((int64_t)kChunk, rest);
-        nrest = rest - nx.d;
-      } else {
-        const QEnt row = ld_qent(hq + rnext);
-        ++rnext;
-        nx.s = row.s;
-        nx.v = row.v;
-        nx.d = min((int32_t)kChunk, row.d);
-        nrest = (int64_t)row.d - nx.d;
+    if (left > 0) {
+      // current slice: row entry `row` (index r), edges [row.s + o, row.s + o + 256) of it
+      int32_t w[kChunkPerLane];
+      // the row's remaining edges after the current slice, and the next row index
+      int64_t rest;   // edges of the current row after this slice
+      uint64_t rnext;  // index of the next row
+      QEnt cur;
+      {
+        uint32_t first;
+        uint64_t r0;
+        const QEnt row = row_of_slice(hq, hs, nrows, i0, &first, &r0);
+        const int64_t off = (int64_t)(i0 - first) * kChunk;
+        cur.s = row.s + off;
+        cur.v = row.v;
+        cur.d = (int32_t)min((int64_t)kChunk, (int64_t)row.d - off);
+        rest = (int64_t)row.d - off - cur.d;
+        rnext = r0 + 1;
+      }
+      columns(cur, w);
+      while (true) {
+        // descriptor of the next slice (same row, or the start of the next row)
+        QEnt nx;
+        nx.s = 0;
+        nx.v = 0;
+        nx.d = 0;
+        int64_t nrest = 0;
+        if (left > 1) {
+          if (rest > 0) {
+            nx.s = cur.s + cur.d;
+            nx.v = cur.v;
+            nx.d = (int32_t)min((int64_t)kChunk, rest);
+            nrest = rest - nx.d;
+          } else {
+            const QEnt row = ld_qent(hq + rnext);
+            ++rnext;
+            nx.s = row.s;
+            nx.v = row.v;
+            nx.d = min((int32_t)kChunk, row.d);
+            nrest = (int64_t)row.d - nx.d;
+          }
+        }
+        int32_t w2[kChunkPerLane];
+        columns(nx, w2);
+        if (lane == 0) acc.scan += (unsigned long long)cur.d;
+        int32_t vv[kChunkPerLane];
+        bool act[kChunkPerLane];
+#pragma unroll
+        for (int k = 0; k < kChunkPerLane; ++k) {
+          vv[k] = cur.v;
+          act[k] = w[k] >= 0;
+        }
+        td_claim<kChunkPerLane>(c, vv, w, act, acc);
+        if (--left == 0) break;
+        cur = nx;
+        rest = nrest;
+#pragma unroll
+        for (int k = 0; k < kChunkPerLane; ++k) w[k] = w2[k];
       }
     }
-    int32_t w2[kChunkPerLane];
-    columns(nx, w2);
-    if (lane == 0) acc.scan += (unsigned long long)cur.d;
-    int32_t vv[kChunkPerLane];
-    bool act[kChunkPerLane];
-#pragma unroll
-    for (int k = 0; k < kChunkPerLane; ++k) {
-      vv[k] = cur.v;
-      act[k] = w[k] >= 0;
-    }
-    td_claim<kChunkPerLane>(c, vv, w, act, acc);
-    if (--left == 0) break;
-    cur = nx;
-    rest = nrest;
-#pragma unroll
-    for (int k = 0; k < kChunkPerLane; ++k) w[k] = w2[k];
+    if (dyn0 >= nh) break;
+    i0 = dyn0 + __shfl_sync(RB_FULL, ticket, 0);
+    if (i0 >= nh) break;
+    if (lane == 0) ticket = atomicAdd(dyn, (unsigned long long)RB_TD_DYN_CHUNK);
+    left = (uint32_t)min((uint64_t)RB_TD_DYN_CHUNK, nh - i0);
   }
 }
 
@@ -1923,7 +1961,7 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
         }
         if (blockIdx.x == 0 && threadIdx.x == 32) t_queue = globaltimer() - t_prev;
         if (p.dbg && blockIdx.x == 0 && threadIdx.x == 0 && done < 64) p.dbg[kDbgPhase + done * 8 + 1] = globaltimer();
-        td_hubs(c, hq, hs, s_ctr[0] >> 40, s_ctr[0] & kSliceMask, acc);
+        td_hubs(c, hq, hs, s_ctr[0] >> 40, s_ctr[0] & kSliceMask, RB_TD_DYN_MINK > 0 ? &in->pad2 : nullptr, acc);
         if (p.dbg && (threadIdx.x & 31) == 0 && done < 64)
           p.dbg[kDbgWarpB + ((uint64_t)done * gridDim.x + blockIdx.x) * kWarps + (threadIdx.x >> 5)] = globaltimer();
       }
@@ -2266,7 +2304,7 @@ __device__ void dist_body(const KParams& p, const XParams& x, int64_t L, int xdi
     if (hubs) {
       const unsigned long long* const src[1] = {&in->hq_count};
       rb::grid_barrier_fetch<1>(p.bar, nblocks, epoch, src, sm.ctr);
-      td_hubs(c, hq, hs, sm.ctr[0] >> 40, sm.ctr[0] & kSliceMask, acc);
+      td_hubs(c, hq, hs, sm.ctr[0] >> 40, sm.ctr[0] & kSliceMask, nullptr, acc);
     }
     if (c.defer) {
       rb::grid_barrier(p.bar, nblocks, epoch);
