@@ -272,6 +272,15 @@ int rb_validate(const int64_t* d_row_starts, const int32_t* d_col, int64_t n, co
                 int64_t source, const int32_t* d_parent, void* d_ws, size_t ws_bytes, int32_t* d_levels,
                 int64_t* h_first_bad, void* stream);
 
+/* ---- sequential BFS parents (_kernels.py:26-54 seq_bfs_kernel) ---------- */
+/* The parent array of the reference's queue BFS from `source` -- parent[w] =
+ * the neighbour that discovers w first in queue order -- computed from the
+ * level array of a level-synchronous traversal (d_level[v] = depth, < 0 for
+ * unreached vertices; n_levels = depth + 1).  Bit-exact with seq_bfs_kernel
+ * for any row order.  d_parent: n int32 (-1 unreached). */
+int rb_bfs_first_parents(const int64_t* d_row_starts, const int32_t* d_col, int64_t n, const int32_t* d_level,
+                         int64_t source, int64_t n_levels, int32_t* d_parent, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -622,14 +622,23 @@ def bfs_run(g: CsrGraph, source: int, params: BfsParams | None = None, g_desc: C
 
 
 def bfs_sequential(g: CsrGraph, source: int) -> BfsResult:
-    """engine.py:440-475 on device: top-down level-synchronous traversal.
-
-    Levels equal the reference's; the parent of each vertex is *a* frontier
-    neighbour (not necessarily the first in scan order)."""
+    """engine.py:440-475 on device: top-down level-synchronous traversal, then
+    the queue BFS's parents (``_kernels.py:26-54``: the neighbour that discovers
+    a vertex first in queue order) from the level array
+    (``rb_bfs_first_parents``), so levels and predecessor equal the reference's."""
     if not 0 <= source < g.n:
         raise ValueError(f"source {source} out of range for n={g.n}")
-    with BfsEngine(g, BfsParams(mode="sequential")) as eng:
+    with BfsEngine(g, BfsParams(mode="sequential"), record_levels=True) as eng:
         res = eng.run(source)
+        if len(res.levels) > 1:  # (an isolated source has no tree to order)
+            torch = _lib.require_cuda()
+            n_dev = eng.n_dev
+            rs, col = g.device_arrays()[:2]
+            par = torch.empty(n_dev, dtype=torch.int32, device="cuda")
+            _lib.check(_lib.lib().rb_bfs_first_parents(_lib.ptr(rs), _lib.ptr(col), n_dev, _lib.ptr(eng.level_device()),
+                                                       int(source), len(res.levels), _lib.ptr(par), _lib.stream_ptr()),
+                       "rb_bfs_first_parents")
+            res.predecessor[:n_dev] = par.cpu().numpy()
     for r in res.levels:
         r.wall_time = 0.0
     return res

@@ -162,6 +162,29 @@ def test_edge_cases(cuda_ok):
         rb.BfsEngine(g, rb.BfsParams(mode="hybrid_reduced"))
 
 
+def test_sequential_parents_equal_reference(cuda_ok, golden_small, ocache):
+    """bfs_sequential's predecessor is the reference's first discoverer
+    (_kernels.py:26-54): against the reference's own bfs_sequential runs
+    (tests/golden/small.npz), and against the pinned oracle on a Kronecker
+    graph with ascending and with degree-sorted rows (any row order)."""
+    for i in range(len(golden_small["n_list"])):
+        n, e = small_graph(golden_small, i)
+        g = oracle.build_csr(n, e)
+        g2 = oracle.apply_permutation(g, oracle.rcm(g)[0])
+        for j, s in enumerate(golden_small[f"g{i}_srcs"]):
+            res = rb.bfs_sequential(to_rb(g2), int(s))
+            assert np.array_equal(res.predecessor, golden_small[f"g{i}_seqpar_{int(s)}"]), (i, int(s))
+    c = ocache.kron(14, 3)
+    g2 = c["g2"]
+    gd = oracle.Csr(g2.n, g2.row_starts, oracle.degree_sort_rows(g2, True), g2.degrees)
+    for g_or in (g2, gd):
+        for s in (0, int(np.argmax(g2.degrees)), c["n_plus"] - 1, g2.n - 1):
+            want_par, want_lev, _, _ = oracle.seq_bfs(g_or, s)
+            res = rb.bfs_sequential(to_rb(g_or), s)
+            assert np.array_equal(res.predecessor, want_par), s
+            assert [r.direction for r in res.levels] == [rb.TOP_DOWN] * len(res.levels)
+
+
 def test_deep_path_continues_past_record_cap(cuda_ok):
     k = 9000  # > 4096 levels per launch -> continuation launches
     e = np.stack([np.arange(k - 1), np.arange(1, k)], 1).astype(np.uint32)
