@@ -1,1 +1,3 @@
-python -m pytest tests/test_gpu_bfs.py -m gpu -x -q -k "sequential or modes or dispatch or small" > gpurun_out/s9_pytest_seq.log 2>&1; tail -15 gpurun_out/s9_pytest_seq.log
+P=paper_2012_10026_b200
+tools/ab.sh "--scale 26 --steps 3 --warmup 3" 2 nopf:RB_LIB=$P/lib_nopf.so pf:RB_LIB=$P/lib_pf.so pf2:RB_LIB=$P/lib_pf2.so
+tools/ab.sh "--graph chunglu --scale 24 --steps 3 --warmup 3" 1 nopf:RB_LIB=$P/lib_nopf.so pf2:RB_LIB=$P/lib_pf2.so
