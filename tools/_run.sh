@@ -1,3 +1,4 @@
-P=paper_2012_10026_b200
-tools/ab.sh "--scale 26 --steps 3 --warmup 3" 2 nopf:RB_LIB=$P/lib_nopf.so pf:RB_LIB=$P/lib_pf.so pf2:RB_LIB=$P/lib_pf2.so
-tools/ab.sh "--graph chunglu --scale 24 --steps 3 --warmup 3" 1 nopf:RB_LIB=$P/lib_nopf.so pf2:RB_LIB=$P/lib_pf2.so
+python bench.py --steps 5 --warmup 3 > gpurun_out/s10_bench.json 2> gpurun_out/s10_bench.err; echo rc=$?
+python -c "
+import json; d=json.load(open('gpurun_out/s10_bench.json')); print(d['value'], d['e2e']['value'], d['clocks'], d['gpu_launches'], d['roofline']['frac'])"
+tail -3 gpurun_out/s10_bench.err
