@@ -1,4 +1,2 @@
-python bench.py --steps 5 --warmup 3 > gpurun_out/s10_bench.json 2> gpurun_out/s10_bench.err; echo rc=$?
-python -c "
-import json; d=json.load(open('gpurun_out/s10_bench.json')); print(d['value'], d['e2e']['value'], d['clocks'], d['gpu_launches'], d['roofline']['frac'])"
-tail -3 gpurun_out/s10_bench.err
+P=paper_2012_10026_b200
+for v in notail tail; do for i in 0 23; do echo "== $v $i"; RB_LIB=$P/lib_$v.so python tools/one_root.py --scale 26 --index $i 2>&1 | tail -10; done; done
