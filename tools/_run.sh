@@ -1,2 +1,3 @@
-P=paper_2012_10026_b200
-for v in notail tail; do for i in 0 23; do echo "== $v $i"; RB_LIB=$P/lib_$v.so python tools/one_root.py --scale 26 --index $i 2>&1 | tail -10; done; done
+bash tools/profile_round2.sh benches launches levels full
+(time python bench.py --impl reference --steps 2 --warmup 1) > gpurun_out/prof2/bench_reference_s26.json 2> gpurun_out/prof2/bench_reference_s26.err; echo ref=$?
+tail -4 gpurun_out/prof2/bench_reference_s26.err
