@@ -281,6 +281,12 @@ int rb_validate(const int64_t* d_row_starts, const int32_t* d_col, int64_t n, co
 int rb_bfs_first_parents(const int64_t* d_row_starts, const int32_t* d_col, int64_t n, const int32_t* d_level,
                          int64_t source, int64_t n_levels, int32_t* d_parent, void* stream);
 
+/* ---- host-side result assembly ------------------------------------------ */
+/* h_dst[0, n) = value with streaming stores from up to `threads` host threads:
+ * the -1 tail of BfsResult.predecessor for the isolated vertices behind n_dev
+ * (engine.py:598), written while the parents are DMA'd into the head. */
+int rb_host_fill_i32(int32_t* h_dst, int64_t n, int32_t value, int threads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -103,6 +103,7 @@ _SIGS = {
     "rb_validate_workspace_bytes": ([I64], SZ),
     "rb_validate": ([P, P, I64, P, I64, P, P, SZ, P, P, P], ctypes.c_int),
     "rb_bfs_first_parents": ([P, P, I64, P, I64, I64, P, P], ctypes.c_int),
+    "rb_host_fill_i32": ([P, I64, ctypes.c_int32, ctypes.c_int], ctypes.c_int),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -1,3 +1,1 @@
-bash tools/profile_round2.sh benches launches levels full
-(time python bench.py --impl reference --steps 2 --warmup 1) > gpurun_out/prof2/bench_reference_s26.json 2> gpurun_out/prof2/bench_reference_s26.err; echo ref=$?
-tail -4 gpurun_out/prof2/bench_reference_s26.err
+python -m pytest tests/test_gpu_bfs.py tests/test_gpu_configs.py -m gpu -x -q > gpurun_out/s12_pytest.log 2>&1; tail -3 gpurun_out/s12_pytest.log
