@@ -326,9 +326,13 @@ class _DeviceBfs:
         _lib.check(L.rb_bfs_results_async(self.h, _lib.ptr(self._state), _lib.ptr(self._recs_pin), _REC_FAST,
                                           dst, chunks, s), "rb_bfs_results_async")
         pt = torch.from_numpy(pred)
-        if n > n_dev:  # the isolated tail, with streaming stores while the GPU works
+        if n - n_dev >= _FILL_STREAM_MIN:
+            # a big isolated tail: streaming stores from a few threads while the GPU works (a cached
+            # fill takes host memory bandwidth from the parents' DMA)
             _lib.check(L.rb_host_fill_i32(ctypes.c_void_p(pred.ctypes.data + 4 * n_dev), n - n_dev, -1, _FILL_THREADS),
                        "rb_host_fill_i32")
+        elif n > n_dev:  # small: torch's resident thread pool (spawning fill threads would cost more)
+            pt[n_dev:].fill_(-1)
         _lib.check(L.rb_bfs_wait(self.h, -1), "rb_bfs_wait")
         nrec = ctypes.c_int64(0)
         done = L.rb_bfs_complete(self.h, _lib.ptr(self._state), _lib.ptr(self._recs_pin), _REC_FAST,
@@ -380,6 +384,7 @@ class _DeviceBfs:
 
 _MAX_CHUNKS = 32  # kMaxChunks of rb_bfs.cu (rb_bfs_results_async)
 _FILL_THREADS = int(os.environ.get("RB_FILL_THREADS", "0")) or min(8, os.cpu_count() or 1)
+_FILL_STREAM_MIN = 8 << 20  # entries (32 MB) from which the tail fill uses rb_host_fill_i32
 _REC_FAST = 64  # level records fetched by the async result path (deeper: drained)
 
 
