@@ -125,6 +125,22 @@ def test_abi_library_exports_header_symbols():
     assert L.rb_rcm_workspace_bytes(1000, 5000) > 0
 
 
+def test_host_fill_streaming_stores():
+    """rb_host_fill_i32 (the -1 tail of BfsResult.predecessor, engine.py:598):
+    unaligned starts, lengths around the 16-entry unroll, one and several threads."""
+    L = _lib.load()
+    rng = np.random.default_rng(5)
+    for n, off, threads in [(0, 0, 1), (1, 1, 1), (15, 3, 4), (16, 0, 1), (17, 2, 8), (1000, 1, 2),
+                            ((3 << 20) + 5, 3, 4), ((2 << 20), 0, 8)]:
+        a = rng.integers(0, 100, size=n + off + 7, dtype=np.int32)
+        want = a.copy()
+        want[off:off + n] = -1
+        rc = L.rb_host_fill_i32(ctypes.c_void_p(a.ctypes.data + 4 * off), n, -1, threads)
+        assert rc == 0 and np.array_equal(a, want), (n, off, threads)
+    assert L.rb_host_fill_i32(None, 10, -1, 1) != 0  # RB_ERR_ARG
+    assert b"rb_host_fill_i32" in L.rb_last_error()
+
+
 def test_no_cpu_fallback_without_cuda():
     import torch
 
