@@ -163,6 +163,21 @@ def require_cuda():
     return torch
 
 
+def workspace(nbytes: int, device="cuda"):
+    """A uint8 CUDA scratch tensor.  Large requests first hand torch's cached
+    but unused blocks back to the driver: at scale 27 the relabel's 96 GB
+    workspace fits the GPU, but not next to 60 GB of cached fragments."""
+    import torch
+
+    if nbytes >= (8 << 30):
+        torch.cuda.empty_cache()
+    try:
+        return torch.empty(nbytes, dtype=torch.uint8, device=device)
+    except torch.OutOfMemoryError:
+        torch.cuda.empty_cache()
+        return torch.empty(nbytes, dtype=torch.uint8, device=device)
+
+
 def stream_ptr():
     import torch
 

@@ -152,7 +152,7 @@ def build_csr(el: EdgeList) -> CsrGraph:
     ed, host = _edges_device(el)
     m = int(ed.shape[0])
     ws_bytes = L.rb_csr_workspace_bytes(m, n)
-    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+    ws = _lib.workspace(ws_bytes)
     md = ctypes.c_int64(0)
     bad = ctypes.c_int64(-1)
     s = _lib.stream_ptr()

@@ -116,7 +116,7 @@ def rcm(g: CsrGraph) -> tuple[Permutation, RcmRunStats]:
     rs, col, deg = g.device_arrays()
     n = g.n
     ws_bytes = L.rb_rcm_workspace_bytes(n, g.m_directed)
-    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+    ws = _lib.workspace(ws_bytes)
     perm = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")[:n]
     inv = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")[:n]
     ranges = torch.empty(2 * max(n, 1), dtype=torch.int64, device="cuda")
@@ -183,7 +183,7 @@ def apply_permutation(g: CsrGraph, perm: Permutation) -> CsrGraph:
     p, inv = perm.device_arrays()
     n, m = g.n, g.m_directed
     ws_bytes = L.rb_permute_workspace_bytes(n, m)
-    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+    ws = _lib.workspace(ws_bytes)
     rs2 = torch.empty(n + 1, dtype=torch.int64, device="cuda")
     col2 = torch.empty(max(m, 1), dtype=torch.int32, device="cuda")[:m]
     deg2 = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")[:n]
@@ -204,7 +204,7 @@ def degree_sort_adjacency(g: CsrGraph, order: str = "descending") -> CsrGraph:
     rs, col, deg = g.device_arrays()
     n, m = g.n, g.m_directed
     ws_bytes = L.rb_permute_workspace_bytes(n, m)
-    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+    ws = _lib.workspace(ws_bytes)
     col2 = torch.empty(max(m, 1), dtype=torch.int32, device="cuda")[:m]
     if m:
         rc = L.rb_degree_sort_adjacency(
