@@ -77,6 +77,9 @@ constexpr int kThreads = RB_THREADS;
 #ifndef RB_BU_PREFETCH
 #define RB_BU_PREFETCH 1  // bottom-up: L2 prefetch of the next step's records while most vertices are unvisited
 #endif
+#ifndef RB_BU_REQUEUE
+#define RB_BU_REQUEUE 1  // bottom-up (large-graph build): continued rows advance one 8-neighbour chunk per batch and are re-queued
+#endif
 #ifndef RB_BU_DEFER_CONT
 #define RB_BU_DEFER_CONT 1  // bottom-up: continuation rows queued per warp and run 32 at a time
 #endif
@@ -113,6 +116,9 @@ constexpr int64_t kBuSparsePs = 2000000; // sparse bottom-up: the list pass (+ c
 constexpr int64_t kSparseRatio = 256;   // sparse bottom-up when at most one vertex in 256 is unvisited
 constexpr int64_t kListRatio = 16;      // a bitmap bottom-up level lists its survivors from one in 16 (list capacity)
 constexpr int kK2 = 258;                         // bottom-up: per-lane checks before the warp takes over
+constexpr int kPairCap = 32 * kBU + 64;           // bottom-up: queued continuation rows per warp
+// per-warp scratch: the row queue (or a top-down row list), then one progress byte per queued row
+constexpr int kPairWords = (kPairCap > kList ? kPairCap : kList) + kPairCap / 4;
 constexpr int kHeavyPerLane = 8;                 // warp-cooperative bottom-up: neighbours per lane per step
 constexpr uint64_t kDbgWarpBase = 65536;  // RB_DEBUG_TS buffer: per-block stamps, then per-warp stamps
 constexpr uint64_t kDbgPhase = 60000;     // RB_DEBUG_TS: CTA 0 phase stamps, 8 per level (top-down sub-phases)
@@ -1173,6 +1179,79 @@ RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uin
     if (pa >= 0) found_one(va, pa, da);
     if (pb >= 0) found_one(vb, pb, db);
   };
+  // One 8-neighbour chunk for each of the top nb (<= 64) queued rows, two per
+  // lane; rows still open afterwards go back on the queue with their progress
+  // (one byte per entry behind the queue), so every batch runs with all lanes
+  // busy -- scanning a row to its end inside the batch kept the warp for the
+  // longest of its 64 rows (35 % of the big level's stall samples sat in that
+  // loop).  Same scan order per row, same checks.  Returns the rows re-queued.
+  uint8_t* const s_prog = reinterpret_cast<uint8_t*>(s_pair + (kPairWords - kPairCap / 4));
+  auto continue_chunk = [&](uint32_t nb) -> uint32_t {
+    const uint32_t base = npend - nb;
+    const bool oa = lane < nb, ob = lane + 32 < nb;
+    const int64_t va = oa ? (int64_t)s_pair[base + lane] : 0, vb = ob ? (int64_t)s_pair[base + lane + 32] : 0;
+    const uint32_t ga = oa ? s_prog[base + lane] : 0u, gb = ob ? s_prog[base + lane + 32] : 0u;
+    __syncwarp();  // every entry is read before survivors are written back
+    const uint32_t da = oa ? (uint32_t)rb::ldg_i32(p.deg + va) : 0u, db = ob ? (uint32_t)rb::ldg_i32(p.deg + vb) : 0u;
+    const int64_t sa = oa ? rb::ldg_i64(p.rs + va) : 0, sb = ob ? rb::ldg_i64(p.rs + vb) : 0;
+    const int64_t la = da < (uint32_t)kK2 ? da : kK2, lb = db < (uint32_t)kK2 ? db : kK2;
+    const int64_t ta = 2 + 8 * (int64_t)ga, tb = 2 + 8 * (int64_t)gb;
+    int32_t pa = -1, pb = -1;
+    uint32_t chk = 0;
+    {
+      int32_t ua[8], ub[8];
+      uint32_t xa[8], xb[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        ua[t] = (oa && ta + t < la) ? rb::ldg_i32(p.col_bu + bu_idx<kRev>(sa, sa + da, ta + t)) : -1;
+        ub[t] = (ob && tb + t < lb) ? rb::ldg_i32(p.col_bu + bu_idx<kRev>(sb, sb + db, tb + t)) : -1;
+      }
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        xa[t] = ua[t] >= 0 ? ld_bits(fcur + (ua[t] >> 5)) : 0u;
+        xb[t] = ub[t] >= 0 ? ld_bits(fcur + (ub[t] >> 5)) : 0u;
+      }
+      chk += chunk_first_hit(ua, xa, pa);
+      chk += chunk_first_hit(ub, xb, pb);
+    }
+    const bool ra = oa && pa < 0 && ta + 8 < la, rb_ = ob && pb < 0 && tb + 8 < lb;  // more chunks to go
+    for (int r = 0; r < 2; ++r) {  // rows past kK2 checks: the whole warp finishes them now
+      const int64_t s0 = r ? sb : sa;
+      const uint32_t d = r ? db : da;
+      int32_t& par = r ? pb : pa;
+      const bool open = r ? (ob && !rb_) : (oa && !ra);
+      uint32_t hm = __ballot_sync(RB_FULL, open && par < 0 && d > (uint32_t)kK2);
+      while (hm) {
+        const int h = __ffs(hm) - 1;
+        hm &= hm - 1;
+        const int64_t hs = rb::shfl_i64(s0, h);
+        const int64_t he = hs + __shfl_sync(RB_FULL, d, h);
+        int64_t hc = 0;
+        const int32_t hp = bu_heavy<kRev>(p, fcur, hs, he, kK2, &hc);
+        if ((int)lane == h) {
+          chk += (uint32_t)hc;
+          par = hp;
+        }
+      }
+    }
+    acc.scan += chk;
+    if (pa >= 0) found_one(va, pa, da);
+    if (pb >= 0) found_one(vb, pb, db);
+    const uint32_t ma = __ballot_sync(RB_FULL, ra), mb = __ballot_sync(RB_FULL, rb_);
+    const uint32_t lt = (1u << lane) - 1u;
+    if (ra) {
+      const uint32_t pos = base + __popc(ma & lt);
+      s_pair[pos] = (uint32_t)va;
+      s_prog[pos] = (uint8_t)(ga + 1);
+    }
+    if (rb_) {
+      const uint32_t pos = base + __popc(ma) + __popc(mb & lt);
+      s_pair[pos] = (uint32_t)vb;
+      s_prog[pos] = (uint8_t)(gb + 1);
+    }
+    __syncwarp();
+    return (uint32_t)(__popc(ma) + __popc(mb));
+  };
 #endif
   auto load_vis = [&](uint64_t w) -> uint32_t {
     return (w < nw && lane < KB) ? __ldcg(p.vis + w + lane) : 0xffffffffu;
@@ -1287,7 +1366,10 @@ RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uin
 #pragma unroll
         for (int k = 0; k < KB; ++k) {  // (unrolled, predicated: no divergent loop)
           const bool q = (needm >> k) & 1u;
-          if (q) s_pair[pos] = (uint32_t)(w0 * 32 + step_off(lane, k));
+          if (q) {
+            s_pair[pos] = (uint32_t)(w0 * 32 + step_off(lane, k));
+            s_prog[pos] = 0;
+          }
           pos += q ? 1u : 0u;
         }
         npend += npairs;
@@ -1299,7 +1381,9 @@ RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uin
         p.vis[w0 + lane] = vw | my_fm;
       }
       __syncwarp();
-      if constexpr (KB == 8) {
+      if constexpr (KB == 8 && RB_BU_REQUEUE) {
+        while (npend >= 64) npend = npend - 64 + continue_chunk(64);  // two rows per lane, one chunk each
+      } else if constexpr (KB == 8) {
         while (npend >= 64) {  // two rows per lane
           npend -= 64;
           continue_batch2(s_pair + npend);
@@ -1401,12 +1485,19 @@ RB_LEVEL_FN void bu_level(const KParams& p, int64_t L, const uint32_t* fcur, uin
     acc.scan += checks;
   }
 #if RB_BU_DEFER_CONT
-  if (!kCollect && npend > 32) {
-    npend -= 32;
-    continue_batch(32, s_pair + npend);
-    __syncwarp();
+  if constexpr (KB == 8 && RB_BU_REQUEUE && !kCollect) {
+    while (npend) {
+      const uint32_t nb = npend < 64u ? npend : 64u;
+      npend = npend - nb + continue_chunk(nb);
+    }
+  } else {
+    if (!kCollect && npend > 32) {
+      npend -= 32;
+      continue_batch(32, s_pair + npend);
+      __syncwarp();
+    }
+    if (!kCollect && npend) continue_batch(npend, s_pair);
   }
-  if (!kCollect && npend) continue_batch(npend, s_pair);
 #endif
 }
 
@@ -1809,7 +1900,7 @@ __global__ void __launch_bounds__(kThreads, RB_MINB) bfs_persistent(KParams p) {
   __shared__ unsigned long long s_red[kWarps * 4];
   __shared__ unsigned long long s_ctr[5];  // [4]: the unvisited list of the last level (bit 40: valid | count)
   __shared__ uint32_t s_bu_found[kWarps][kBU];
-  __shared__ uint32_t s_bu_pair[kWarps][32 * kBU + 64 > kList ? 32 * kBU + 64 : kList];
+  __shared__ uint32_t s_bu_pair[kWarps][kPairWords];
   __shared__ uint32_t s_bu_next[2];  // bottom-up: next step of this CTA (level parity)
   __shared__ SoloShared s_solo;
   __shared__ uint32_t s_wtot[32];
@@ -2271,7 +2362,7 @@ struct DistShared {
   unsigned long long red[kWarps * 4];
   unsigned long long ctr[5];
   uint32_t bu_found[kWarps][kBU];
-  uint32_t bu_pair[kWarps][32 * kBU + 64 > kList ? 32 * kBU + 64 : kList];
+  uint32_t bu_pair[kWarps][kPairWords];
   uint32_t next_step;
 };
 
